@@ -1,0 +1,172 @@
+// common.cuh — device-side building blocks shared by every kernel family:
+// hash functions, 64-bit atomics, TMA bulk copies
+// and mbarriers (sm_90+/sm_100a), warp helpers.
+#pragma once
+
+#include <cstdint>
+
+#include "hawk_b200.h"
+
+namespace hk {
+
+using u64 = unsigned long long;
+using i64 = long long;
+
+constexpr u64 kEmpty = 0x8000000000000000ull;  // HAWK_EMPTY_KEY
+constexpr u64 kBusy = 2ull;                    // aggregation slot being claimed
+
+// ---- hashing ---------------------------------------
+
+__host__ __device__ __forceinline__ u64 fmix64(u64 k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdull;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ull;
+  k ^= k >> 33;
+  return k;
+}
+
+// slot in [0, 2^log2cap). Murmur: fmix64(x ^ seed) masked; multiply-shift:
+// (a*x mod 2^64) >> (64 - b) with a = seed | 1 (odd), b = log2cap >= 1.
+template <int HFN>
+__host__ __device__ __forceinline__ u64 hash_slot(u64 x, u64 seed, int log2cap) {
+  if (HFN == HAWK_MURMUR) return fmix64(x ^ seed) & ((1ull << log2cap) - 1ull);
+  return ((seed | 1ull) * x) >> (64 - log2cap);
+}
+
+__host__ __device__ __forceinline__ u64 hash_dispatch(int fn, u64 x, u64 seed, int log2cap) {
+  return fn == HAWK_MURMUR ? hash_slot<HAWK_MURMUR>(x, seed, log2cap)
+                           : hash_slot<HAWK_MULTIPLY_SHIFT>(x, seed, log2cap);
+}
+
+// Combines a composite group key into one 64-bit word before hashing.
+__host__ __device__ __forceinline__ u64 combine_key(u64 h, u64 k) {
+  return fmix64(h + 0x9e3779b97f4a7c15ull) ^ k;
+}
+
+// ---- bit casts ---------------------------------------------------------------
+
+__device__ __forceinline__ double as_f64(u64 b) { return __longlong_as_double((i64)b); }
+__device__ __forceinline__ u64 as_bits(double d) { return (u64)__double_as_longlong(d); }
+
+// ---- loads ---------------------------------------------------------------------
+
+__device__ __forceinline__ u64 ldg64(const void* p) {
+  return (u64)__ldg(reinterpret_cast<const i64*>(p));
+}
+__device__ __forceinline__ void ldg128(const void* p, u64& a, u64& b) {
+  longlong2 v = __ldg(reinterpret_cast<const longlong2*>(p));
+  a = (u64)v.x;
+  b = (u64)v.y;
+}
+__device__ __forceinline__ u64 ld_volatile(const u64* p) {
+  return *reinterpret_cast<const volatile u64*>(p);
+}
+
+// ---- atomics on generic addresses (smem or HBM) -------------------------------
+
+__device__ __forceinline__ u64 atomic_cas(u64* p, u64 cmp, u64 val) { return atomicCAS(p, cmp, val); }
+__device__ __forceinline__ void atomic_add_i(u64* p, u64 v) { atomicAdd(p, v); }
+__device__ __forceinline__ void atomic_add_f(u64* p, double v) {
+  atomicAdd(reinterpret_cast<double*>(p), v);
+}
+__device__ __forceinline__ void atomic_min_i(u64* p, u64 v) {
+  atomicMin(reinterpret_cast<i64*>(p), (i64)v);
+}
+__device__ __forceinline__ void atomic_max_i(u64* p, u64 v) {
+  atomicMax(reinterpret_cast<i64*>(p), (i64)v);
+}
+__device__ __forceinline__ void atomic_min_f(u64* p, double v) {
+  u64 old = ld_volatile(p);
+  while (v < as_f64(old)) {
+    u64 prev = atomicCAS(p, old, as_bits(v));
+    if (prev == old) break;
+    old = prev;
+  }
+}
+__device__ __forceinline__ void atomic_max_f(u64* p, double v) {
+  u64 old = ld_volatile(p);
+  while (v > as_f64(old)) {
+    u64 prev = atomicCAS(p, old, as_bits(v));
+    if (prev == old) break;
+    old = prev;
+  }
+}
+
+// 128-bit atomic exchange of a {key, payload} join slot (cuckoo eviction).
+__device__ __forceinline__ void atomic_exch128(u64* p, u64& key, u64& payload) {
+  asm volatile(
+      "{\n\t.reg .b128 d, s;\n\t"
+      "mov.b128 s, {%2, %3};\n\t"
+      "atom.global.exch.b128 d, [%4], s;\n\t"
+      "mov.b128 {%0, %1}, d;\n\t}"
+      : "=l"(key), "=l"(payload)
+      : "l"(key), "l"(payload), "l"(p)
+      : "memory");
+}
+
+// ---- TMA bulk copies + mbarriers (cp.async.bulk, sm_90+) ------------------
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy completing on `bar` (bytes % 16 == 0, 16B aligned)
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+// ---- warp helpers ------------------------------------------------------------
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// Member mask of the calling thread's warp: blocks may be smaller than a
+// warp (work_group_size 16, thread_multiplier 1), so the last warp can be
+// partial. Members are always lanes 0..n-1.
+__device__ __forceinline__ unsigned warp_mask() {
+  const int rem = (int)blockDim.x - (int)(threadIdx.x & ~31u);
+  return rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
+}
+__device__ __forceinline__ int warp_size_here() {
+  const int rem = (int)blockDim.x - (int)(threadIdx.x & ~31u);
+  return rem >= 32 ? 32 : rem;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v, unsigned mask) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T n = __shfl_up_sync(mask, v, o);
+    if (lane_id() >= o) v += n;
+  }
+  return v;
+}
+
+}  // namespace hk

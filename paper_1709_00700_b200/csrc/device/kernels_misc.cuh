@@ -1,0 +1,146 @@
+// kernels_misc.cuh — small kernels around the pipeline kernels: exclusive
+// scans, standalone table build/probe, cuckoo
+// duplicate check, aggregation-table extract/merge (HostMergeHashTables,
+// SPEC.md:287), data generation (include/hawk_gen.h).
+#pragma once
+
+#include "hawk_gen.h"
+#include "pipeline_kernel.cuh"
+
+namespace hk {
+
+// ---- exclusive prefix sum (3 phases: block scan, scan of block sums, add) -----
+
+constexpr int kScanBlock = 512;
+constexpr int kScanItems = 8;  // elements per thread per block pass
+
+__global__ void __launch_bounds__(kScanBlock)
+    scan_blocks_kernel(const int64_t* in, int64_t n, int64_t* out, int64_t* block_sums) {
+  __shared__ u64 scratch[40];
+  const int64_t base = (int64_t)blockIdx.x * kScanBlock * kScanItems;
+  u64 v[kScanItems];
+  u64 local = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int64_t idx = base + (int64_t)threadIdx.x * kScanItems + i;
+    v[i] = idx < n ? (u64)in[idx] : 0ull;
+    local += v[i];
+  }
+  u64 total;
+  u64 excl = block_exclusive_scan(local, scratch, total);
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int64_t idx = base + (int64_t)threadIdx.x * kScanItems + i;
+    if (idx < n) out[idx] = (int64_t)excl;
+    excl += v[i];
+  }
+  if (threadIdx.x == 0) block_sums[blockIdx.x] = (int64_t)total;
+}
+
+// single-CTA exclusive scan of up to any length (loops); writes the total.
+__global__ void __launch_bounds__(1024)
+    scan_single_kernel(int64_t* data, int64_t n, int64_t* total_out) {
+  __shared__ u64 scratch[40];
+  u64 carry = 0;
+  for (int64_t base = 0; base < n; base += blockDim.x) {
+    const int64_t idx = base + threadIdx.x;
+    const u64 v = idx < n ? (u64)data[idx] : 0ull;
+    u64 total;
+    const u64 excl = block_exclusive_scan(v, scratch, total);
+    if (idx < n) data[idx] = (int64_t)(carry + excl);
+    carry += total;
+  }
+  if (threadIdx.x == 0 && total_out) *total_out = (int64_t)carry;
+}
+
+__global__ void scan_add_kernel(int64_t* out, int64_t n, const int64_t* block_offsets) {
+  const int64_t base = (int64_t)blockIdx.x * kScanBlock * kScanItems;
+  const int64_t add = block_offsets[blockIdx.x];
+  for (int i = threadIdx.x; i < kScanBlock * kScanItems; i += blockDim.x) {
+    const int64_t idx = base + i;
+    if (idx < n) out[idx] += add;
+  }
+}
+
+// ---- join tables ----------------------------------------------------------------
+
+__global__ void fill_kernel(u64* p, u64 value, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = value;
+}
+
+template <int IMPL, int HFN>
+__global__ void table_insert_kernel(hawk_table t, const int64_t* keys, const int64_t* payloads,
+                                    int64_t n, int* flags) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    table_insert<IMPL, HFN>(t, (u64)keys[i], payloads ? (u64)payloads[i] : (u64)i, flags);
+}
+
+template <int IMPL, int HFN>
+__global__ void table_probe_kernel(hawk_table t, const int64_t* keys, int64_t n, int64_t* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = table_find<IMPL, HFN>(t, (u64)keys[i]);
+}
+
+// A cuckoo key can only live at T1[h1(k)] or T2[h2(k)]; a duplicate build
+// key therefore shows up as the same key in both candidate slots.
+template <int HFN>
+__global__ void cuckoo_duplicate_kernel(hawk_table t, int* flags) {
+  const u64* s = reinterpret_cast<const u64*>(t.d_slots);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < t.capacity;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const u64 k = s[2 * i];
+    if (k == kEmpty) continue;
+    const u64 j = hash_slot<HFN>(k, t.seed[1], t.log2_capacity);
+    if (s[2 * ((u64)t.capacity + j)] == k) atomicOr(flags, HAWK_FLAG_DUPLICATE);
+  }
+}
+
+// ---- aggregation tables -------------------------------------------------------------
+
+// Compacts occupied slots into rows of (keys..., accs...).
+__global__ void agg_extract_kernel(const u64* slots, int64_t nslots, int K, int A, int64_t* out,
+                                   u64* cursor) {
+  const int words = 1 + K + A;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nslots;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const u64* sl = slots + i * words;
+    if ((sl[0] & 1ull) == 0ull) continue;  // EMPTY (0) / never BUSY after the kernel
+    const u64 pos = atomicAdd(cursor, 1ull);
+    for (int w = 0; w < K + A; ++w) out[pos * (K + A) + w] = (int64_t)sl[1 + w];
+  }
+}
+
+// Merges partial group rows (keys..., accs...) into a table (multi-GPU merge).
+template <int IMPL, int HFN>
+__global__ void agg_merge_rows_kernel(const __grid_constant__ KParams kp, const int64_t* rows,
+                                      int64_t n) {
+  const hawk_pipeline& p = kp.p;
+  const int K = p.nkeys, A = p.naggs;
+  const hawk_table& gt = p.sink_table;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const u64* r = reinterpret_cast<const u64*>(rows + i * (K + A));
+    u64* g = agg_find_or_insert<IMPL, HFN, false>(kp, reinterpret_cast<u64*>(gt.d_slots),
+                                                 gt.log2_capacity, gt.seed, r, 1, kp.d_cursor);
+    if (!g) {
+      atomicOr(kp.d_flags, HAWK_FLAG_TABLE_FULL);
+      continue;
+    }
+    for (int a = 0; a < A; ++a) agg_merge(g + 1 + K + a, p.aggs[a].fn, p.aggs[a].type, r[K + a]);
+  }
+}
+
+// ---- synthetic data ---------------------------------------------------------------
+
+__global__ void gen_column_kernel(int table, int col, double sf, uint64_t seed, int64_t row_begin,
+                                  int64_t n, int64_t* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = hg_value(table, col, row_begin + i, sf, seed);
+}
+
+}  // namespace hk

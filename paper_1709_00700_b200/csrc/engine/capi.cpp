@@ -1,0 +1,359 @@
+// capi.cpp — extern "C" wrapper of the C++ engine (include/hawk_b200_engine.h).
+// No exception crosses this boundary: each is mapped to its hawk_status class.
+#include <cstring>
+#include <sstream>
+
+#include "hawk/sql/parser.hpp"
+#include "hawk_b200_engine.h"
+#include "hawk_b200_engine.hpp"
+
+using namespace hawk;
+using namespace hawk::b200;
+
+struct hawk_engine {
+  Engine engine;
+  explicit hawk_engine(int d) : engine(d) {}
+};
+
+struct hawk_result {
+  Table table{"result", {}};
+  ExecutionMetrics metrics;
+  std::string metrics_text;
+};
+
+struct hawk_partial {
+  PartialResult part;
+  double kernel_ms = 0;
+};
+
+namespace {
+
+thread_local std::string g_error;
+thread_local int32_t g_error_class = 0;
+
+int32_t classify(const std::exception& e) {
+  if (dynamic_cast<const UnsupportedPlan*>(&e)) return HAWK_ERR_UNSUPPORTED_PLAN;
+  if (dynamic_cast<const InvalidConfig*>(&e)) return HAWK_ERR_INVALID_CONFIG;
+  if (dynamic_cast<const Unsupported*>(&e)) return HAWK_ERR_UNSUPPORTED;
+  if (dynamic_cast<const PlanTooLarge*>(&e)) return HAWK_ERR_PLAN_TOO_LARGE;
+  if (dynamic_cast<const CapacityExceeded*>(&e)) return HAWK_ERR_CAPACITY;
+  if (dynamic_cast<const DuplicateKey*>(&e)) return HAWK_ERR_DUPLICATE_KEY;
+  if (dynamic_cast<const EmptyAggregate*>(&e)) return HAWK_ERR_EMPTY_AGGREGATE;
+  if (dynamic_cast<const DivergentPlan*>(&e)) return HAWK_ERR_DIVERGENT_PLAN;
+  if (dynamic_cast<const InvalidParams*>(&e)) return HAWK_ERR_INVALID_PARAMS;
+  // front-end errors: 10 SyntaxError, 11 UnknownTable, 12 UnknownAttribute, 13 TypeError
+  if (dynamic_cast<const SyntaxError*>(&e)) return 10;
+  if (dynamic_cast<const UnknownTable*>(&e)) return 11;
+  if (dynamic_cast<const UnknownAttribute*>(&e)) return 12;
+  if (dynamic_cast<const TypeError*>(&e)) return 13;
+  return 99;
+}
+
+template <typename F>
+int32_t guard(F&& f) {
+  try {
+    f();
+    g_error.clear();
+    g_error_class = 0;
+    return HAWK_OK;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    g_error_class = classify(e);
+    return g_error_class;
+  } catch (...) {
+    g_error = "unknown error";
+    g_error_class = 99;
+    return 99;
+  }
+}
+
+PipelineSet plan_sql(Engine& engine, const std::string& sql) {
+  const std::vector<TablePtr> tables = engine.catalog();
+  auto plan = sql::parse_query(sql, sql::make_catalog(tables));
+  return partition_into_pipelines(plan, tables);
+}
+
+// "<proj>;<agg>" workload config, or "c0|c1|..." one per pipeline
+std::vector<VariantConfiguration> configs_for(const PipelineSet& set, const std::string& text) {
+  std::vector<VariantConfiguration> out;
+  if (text.find('|') != std::string::npos) {
+    std::stringstream ss(text);
+    std::string part;
+    while (std::getline(ss, part, '|')) out.push_back(parse_variant(part));
+    if (out.size() != set.pipelines.size()) throw InvalidConfig("one configuration per pipeline required");
+    return out;
+  }
+  WorkloadConfig w = text.empty() ? WorkloadConfig() : parse_workload_config(text);
+  for (const PipelineProgram& p : set.pipelines)
+    out.push_back(p.kind == PipelineKind::Projection ? w.projection : w.aggregation);
+  return out;
+}
+
+void fill_metrics_text(hawk_result* r) {
+  std::ostringstream os;
+  for (const PipelineMetrics& p : r->metrics.pipelines)
+    os << p.variant << ' ' << p.kernel_ms << ' ' << p.launches << ' ' << p.rows_in << ' '
+       << p.rows_out << ' ' << p.grid << ' ' << p.block << ' ' << p.retries << '\n';
+  r->metrics_text = os.str();
+}
+
+void put_str(char* buf, int32_t len, const std::string& s) {
+  if (!buf || len <= 0) return;
+  std::strncpy(buf, s.c_str(), static_cast<std::size_t>(len - 1));
+  buf[len - 1] = 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hawk_engine_last_error(void) { return g_error.c_str(); }
+int32_t hawk_engine_last_error_class(void) { return g_error_class; }
+
+int32_t hawk_engine_create(int32_t device, hawk_engine** out) {
+  return guard([&] { *out = new hawk_engine(device); });
+}
+
+void hawk_engine_destroy(hawk_engine* e) { delete e; }
+
+int32_t hawk_engine_sm_count(hawk_engine* e) { return e->engine.sm_count(); }
+void* hawk_engine_ctx(hawk_engine* e) { return e->engine.ctx(); }
+
+int32_t hawk_engine_put_columns(hawk_engine* e, const char* name, int32_t ncols,
+                                const char* const* names, const int32_t* kinds, int64_t rows,
+                                const void* const* data, const char* const* const* lexicons,
+                                const int64_t* lexicon_sizes, const int64_t* distinct,
+                                int64_t row_offset) {
+  return guard([&] {
+    Schema schema;
+    std::vector<const void*> cols;
+    std::vector<std::vector<std::string>> lex(static_cast<std::size_t>(ncols));
+    std::vector<int64_t> dist;
+    for (int c = 0; c < ncols; ++c) {
+      schema.push_back({names[c], static_cast<ColumnKind>(kinds[c])});
+      cols.push_back(data[c]);
+      if (kinds[c] == 2 && lexicons && lexicon_sizes)
+        for (int64_t i = 0; i < lexicon_sizes[c]; ++i) lex[static_cast<std::size_t>(c)].emplace_back(lexicons[c][i]);
+      dist.push_back(distinct ? distinct[c] : 0);
+    }
+    e->engine.put_columns(name, schema, rows, cols, lex, dist, row_offset);
+  });
+}
+
+int32_t hawk_engine_generate(hawk_engine* e, int32_t table, double sf, uint64_t seed,
+                             int64_t row_begin, int64_t rows) {
+  return guard([&] { e->engine.generate_table(table, sf, seed, row_begin, rows); });
+}
+
+int32_t hawk_engine_drop(hawk_engine* e, const char* name) {
+  return guard([&] { e->engine.drop_table(name); });
+}
+
+int64_t hawk_engine_table_rows(hawk_engine* e, const char* name) {
+  if (!e->engine.has_table(name)) return -1;
+  return e->engine.table(name).rows;
+}
+
+const int64_t* hawk_engine_column(hawk_engine* e, const char* table, const char* column) {
+  if (!e->engine.has_table(table)) return nullptr;
+  const DeviceTable& t = e->engine.table(table);
+  const int c = t.find(column);
+  return c < 0 ? nullptr : t.columns[static_cast<std::size_t>(c)].d_data;
+}
+
+int32_t hawk_engine_flush_l2(hawk_engine* e) {
+  return guard([&] { e->engine.flush_l2(); });
+}
+
+int32_t hawk_engine_run(hawk_engine* e, const char* sql, const char* config, hawk_result** out) {
+  *out = nullptr;
+  return guard([&] {
+    PipelineSet set = plan_sql(e->engine, sql);
+    auto configs = configs_for(set, config ? config : "");
+    auto* r = new hawk_result;
+    try {
+      r->table = e->engine.execute(set, configs, &r->metrics);
+    } catch (...) {
+      delete r;
+      throw;
+    }
+    fill_metrics_text(r);
+    *out = r;
+  });
+}
+
+int32_t hawk_engine_run_partial(hawk_engine* e, const char* sql, const char* config,
+                                hawk_partial** out) {
+  *out = nullptr;
+  return guard([&] {
+    PipelineSet set = plan_sql(e->engine, sql);
+    WorkloadConfig w = config && *config ? parse_workload_config(config) : WorkloadConfig();
+    auto* p = new hawk_partial;
+    ExecutionMetrics m;
+    try {
+      p->part = e->engine.execute_partial(set, w, &m);
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    p->kernel_ms = m.kernel_ms;
+    *out = p;
+  });
+}
+
+int64_t hawk_partial_rows(const hawk_partial* p) { return p->part.rows; }
+int32_t hawk_partial_width(const hawk_partial* p) { return p->part.width; }
+int32_t hawk_partial_sink(const hawk_partial* p) { return p->part.sink; }
+const int64_t* hawk_partial_data(const hawk_partial* p) { return p->part.values.data(); }
+double hawk_partial_kernel_ms(const hawk_partial* p) { return p->kernel_ms; }
+void hawk_partial_free(hawk_partial* p) { delete p; }
+
+int32_t hawk_engine_finalize(hawk_engine* e, const char* sql, const char* config, int32_t nparts,
+                             const int64_t* const* data, const int64_t* rows, hawk_result** out) {
+  *out = nullptr;
+  return guard([&] {
+    PipelineSet set = plan_sql(e->engine, sql);
+    WorkloadConfig w = config && *config ? parse_workload_config(config) : WorkloadConfig();
+    // widths come from the lowered terminal program
+    const std::size_t T = static_cast<std::size_t>(set.terminal);
+    PipelineProgram term = apply_variant(set.pipelines[T], set.pipelines[T].kind == PipelineKind::Projection
+                                                               ? w.projection
+                                                               : w.aggregation);
+    LoweredProgram lp = lower_program(term, set);
+    int width = lp.pipe.sink == HAWK_SINK_AGGREGATE   ? lp.pipe.naggs
+                : lp.pipe.sink == HAWK_SINK_PROJECT ? lp.pipe.nproject
+                                                    : lp.pipe.nkeys + lp.pipe.naggs;
+    std::vector<PartialResult> parts(static_cast<std::size_t>(nparts));
+    for (int i = 0; i < nparts; ++i) {
+      PartialResult& p = parts[static_cast<std::size_t>(i)];
+      p.sink = lp.pipe.sink;
+      p.rows = rows[i];
+      p.width = width;
+      p.values.assign(data[i], data[i] + rows[i] * width);
+    }
+    auto* r = new hawk_result;
+    try {
+      r->table = e->engine.finalize_partials(set, w, parts);
+    } catch (...) {
+      delete r;
+      throw;
+    }
+    *out = r;
+  });
+}
+
+int64_t hawk_result_rows(const hawk_result* r) { return static_cast<int64_t>(r->table.row_count()); }
+int32_t hawk_result_ncols(const hawk_result* r) { return static_cast<int32_t>(r->table.column_count()); }
+const char* hawk_result_col_name(const hawk_result* r, int32_t c) {
+  return r->table.column_name(static_cast<std::size_t>(c)).c_str();
+}
+int32_t hawk_result_col_kind(const hawk_result* r, int32_t c) {
+  return static_cast<int32_t>(r->table.column(static_cast<std::size_t>(c)).kind());
+}
+const void* hawk_result_col_data(const hawk_result* r, int32_t c) {
+  const Column& col = r->table.column(static_cast<std::size_t>(c));
+  if (col.kind() == ColumnKind::Float64) return col.floats().data();
+  return col.ints().data();
+}
+int64_t hawk_result_col_lexicon_size(const hawk_result* r, int32_t c) {
+  return static_cast<int64_t>(r->table.column(static_cast<std::size_t>(c)).lexicon().size());
+}
+const char* hawk_result_col_lexicon(const hawk_result* r, int32_t c, int64_t i) {
+  return r->table.column(static_cast<std::size_t>(c)).lexicon()[static_cast<std::size_t>(i)].c_str();
+}
+double hawk_result_kernel_ms(const hawk_result* r) { return r->metrics.kernel_ms; }
+double hawk_result_wall_ms(const hawk_result* r) { return r->metrics.wall_ms; }
+int64_t hawk_result_input_tuples(const hawk_result* r) { return r->metrics.input_tuples; }
+int32_t hawk_result_launches(const hawk_result* r) { return r->metrics.launches; }
+const char* hawk_result_metrics_text(const hawk_result* r) { return r->metrics_text.c_str(); }
+void hawk_result_free(hawk_result* r) { delete r; }
+
+int32_t hawk_engine_pipeline_count(hawk_engine* e, const char* sql, int32_t* n) {
+  return guard([&] { *n = static_cast<int32_t>(plan_sql(e->engine, sql).pipelines.size()); });
+}
+
+int32_t hawk_engine_space_size(hawk_engine* e, const char* sql, int32_t pipeline, int32_t* n,
+                               int32_t* single_pass) {
+  return guard([&] {
+    PipelineSet set = plan_sql(e->engine, sql);
+    auto space = enumerate_variant_space(set.pipelines.at(static_cast<std::size_t>(pipeline)));
+    *n = static_cast<int32_t>(space.size());
+    *single_pass = 0;
+    for (const auto& c : space) *single_pass += c.strategy == Strategy::SinglePass;
+  });
+}
+
+int32_t hawk_engine_space_config(hawk_engine* e, const char* sql, int32_t pipeline, int32_t i,
+                                 char* buf, int32_t len) {
+  return guard([&] {
+    PipelineSet set = plan_sql(e->engine, sql);
+    auto space = enumerate_variant_space(set.pipelines.at(static_cast<std::size_t>(pipeline)));
+    put_str(buf, len, space.at(static_cast<std::size_t>(i)).to_string());
+  });
+}
+
+int32_t hawk_engine_validate(hawk_engine* e, const char* sql, const char* config, char* buf,
+                             int32_t len) {
+  return guard([&] {
+    PipelineSet set = plan_sql(e->engine, sql);
+    auto configs = configs_for(set, config ? config : "");
+    std::vector<HashTableDescriptor> desc;
+    std::vector<PipelineProgram> progs = apply_variants(set, configs, desc);
+    std::ostringstream os;
+    for (std::size_t i = 0; i < progs.size(); ++i)
+      for (const Diagnostic& d : validate_program(progs[i], &desc))
+        os << i << ':' << d.code << ':' << d.message << '\n';
+    put_str(buf, len, os.str());
+  });
+}
+
+int32_t hawk_engine_explain(hawk_engine* e, const char* sql, const char* config, char* buf,
+                            int32_t len) {
+  return guard([&] {
+    PipelineSet set = plan_sql(e->engine, sql);
+    auto configs = configs_for(set, config ? config : "");
+    std::ostringstream os;
+    for (std::size_t i = 0; i < set.pipelines.size(); ++i) {
+      PipelineProgram prog = apply_variant(set.pipelines[i], configs[i]);
+      LoweredProgram lp = lower_program(prog, set);
+      os << "pipeline " << i << (static_cast<int>(i) == set.terminal ? " (terminal)" : "") << " driver "
+         << set.tables.at(static_cast<std::size_t>(prog.driver_table))->name() << " ["
+         << configs[i].to_string() << "]\n"
+         << describe(lp.pipe);
+    }
+    put_str(buf, len, os.str());
+  });
+}
+
+int32_t hawk_engine_measure(hawk_engine* e, const char* const* sqls, int32_t n, const char* config,
+                            double prune_ms, int32_t reps, double* ms) {
+  return guard([&] {
+    std::vector<WorkloadQuery> w;
+    for (int i = 0; i < n; ++i) w.push_back({"q" + std::to_string(i), sqls[i]});
+    LearnOptions opt;
+    opt.prune_threshold_ms = prune_ms;
+    opt.repetitions = reps;
+    Measurement m = measure_variant(e->engine, parse_workload_config(config), w, opt);
+    *ms = m.ms;
+  });
+}
+
+int32_t hawk_engine_learn(hawk_engine* e, const char* const* sqls, int32_t n, int32_t q,
+                          double prune_ms, int32_t reps, char* best, int32_t len, double* best_ms,
+                          int32_t* evaluations, int32_t* sweeps) {
+  return guard([&] {
+    std::vector<WorkloadQuery> w;
+    for (int i = 0; i < n; ++i) w.push_back({"q" + std::to_string(i), sqls[i]});
+    LearnOptions opt;
+    opt.max_iterations = q;
+    opt.prune_threshold_ms = prune_ms;
+    opt.repetitions = reps;
+    LearnResult r = learn_variant_configuration(e->engine, w, opt);
+    put_str(best, len, r.best.to_string());
+    *best_ms = r.best_ms;
+    *evaluations = r.evaluations;
+    *sweeps = r.sweeps;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,316 @@
+"""Python host mirror of the engine's C ABI (include/hawk_b200_engine.h).
+
+Mirrors the reference CLI's `run` / `explore` / `learn` operations
+ with the reference's error classes
+(/root/reference/proj/include/hawk/error.hpp:9-54) raised as Python
+exceptions of the same names. All work happens in libhawk_engine.so and the
+sm_100a kernels of libhawk_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+
+# ---- reference exception classes (hawk/error.hpp) ------------------------------
+
+
+class HawkError(RuntimeError):
+    code = 99
+
+
+class UnsupportedPlan(HawkError):
+    code = 1
+
+
+class InvalidConfig(HawkError):
+    code = 2
+
+
+class Unsupported(HawkError):
+    code = 3
+
+
+class PlanTooLarge(HawkError):
+    code = 4
+
+
+class CapacityExceeded(HawkError):
+    code = 5
+
+
+class DuplicateKey(HawkError):
+    code = 6
+
+
+class EmptyAggregate(HawkError):
+    code = 7
+
+
+class DivergentPlan(HawkError):
+    code = 8
+
+
+class InvalidParams(HawkError):
+    code = 9
+
+
+class SyntaxError_(HawkError):
+    code = 10
+
+
+class UnknownTable(HawkError):
+    code = 11
+
+
+class UnknownAttribute(HawkError):
+    code = 12
+
+
+class TypeError_(HawkError):
+    code = 13
+
+
+_BY_CODE = {c.code: c for c in (UnsupportedPlan, InvalidConfig, Unsupported, PlanTooLarge,
+                                CapacityExceeded, DuplicateKey, EmptyAggregate, DivergentPlan,
+                                InvalidParams, SyntaxError_, UnknownTable, UnknownAttribute,
+                                TypeError_)}
+ERROR_NAMES = {1: "UnsupportedPlan", 2: "InvalidConfig", 3: "Unsupported", 4: "PlanTooLarge",
+               5: "CapacityExceeded", 6: "DuplicateKey", 7: "EmptyAggregate",
+               8: "DivergentPlan", 9: "InvalidParams", 10: "SyntaxError", 11: "UnknownTable",
+               12: "UnknownAttribute", 13: "TypeError"}
+
+
+def _raise(status: int):
+    lib = _native.engine()
+    msg = lib.hawk_engine_last_error().decode(errors="replace")
+    raise _BY_CODE.get(status, HawkError)(msg)
+
+
+def _check(status: int):
+    if status != 0:
+        _raise(status)
+
+
+INT64, FLOAT64, STRING = 0, 1, 2
+
+
+@dataclass
+class Column:
+    name: str
+    kind: int
+    values: np.ndarray            # int64 / float64 / int64 codes
+    lexicon: list[str] | None = None
+
+    def decoded(self) -> list:
+        if self.kind == STRING:
+            return [self.lexicon[c] for c in self.values]
+        return self.values.tolist()
+
+
+@dataclass
+class Result:
+    columns: list[Column]
+    kernel_ms: float
+    wall_ms: float
+    input_tuples: int
+    launches: int
+    pipelines: list[dict] = field(default_factory=list)
+
+    @property
+    def rows(self) -> int:
+        return len(self.columns[0].values) if self.columns else 0
+
+    def column(self, name: str) -> Column:
+        for c in self.columns:
+            if c.name == name:
+                return c
+        raise KeyError(name)
+
+
+def _result_from(lib, r) -> Result:
+    cols = []
+    n = lib.hawk_result_rows(r)
+    for c in range(lib.hawk_result_ncols(r)):
+        kind = lib.hawk_result_col_kind(r, c)
+        name = lib.hawk_result_col_name(r, c).decode()
+        ptr = lib.hawk_result_col_data(r, c)
+        dtype = np.float64 if kind == FLOAT64 else np.int64
+        vals = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_double if kind == FLOAT64 else C.c_int64)),
+                                     shape=(n,)).copy() if n else np.zeros(0, dtype)
+        lex = None
+        if kind == STRING:
+            lex = [lib.hawk_result_col_lexicon(r, c, i).decode()
+                   for i in range(lib.hawk_result_col_lexicon_size(r, c))]
+        cols.append(Column(name, kind, vals, lex))
+    pipes = []
+    for line in lib.hawk_result_metrics_text(r).decode().splitlines():
+        p = line.split()
+        if len(p) >= 8:
+            pipes.append(dict(variant=p[0], kernel_ms=float(p[1]), launches=int(p[2]),
+                              rows_in=int(p[3]), rows_out=int(p[4]), grid=int(p[5]),
+                              block=int(p[6]), retries=int(p[7])))
+    return Result(cols, lib.hawk_result_kernel_ms(r), lib.hawk_result_wall_ms(r),
+                  lib.hawk_result_input_tuples(r), lib.hawk_result_launches(r), pipes)
+
+
+class Engine:
+    """One B200 engine (device column store + executor). device < 0 gives a
+    planning-only engine: catalog, passes, variant space, lowering; no GPU."""
+
+    def __init__(self, device: int = 0):
+        self._lib = _native.engine()
+        h = C.c_void_p()
+        _check(self._lib.hawk_engine_create(device, C.byref(h)))
+        self._h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.hawk_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def sm_count(self) -> int:
+        return self._lib.hawk_engine_sm_count(self._h)
+
+    @property
+    def ctx(self) -> int:
+        return self._lib.hawk_engine_ctx(self._h)
+
+    # ---- tables ----
+    def put_table(self, name: str, columns: list[Column], distinct: list[int] | None = None,
+                  row_offset: int = 0):
+        """Uploads host columns (H2D); string columns are codes + lexicon."""
+        n = len(columns[0].values) if columns else 0
+        keep = []
+        names = (C.c_char_p * len(columns))(*[c.name.encode() for c in columns])
+        kinds = (C.c_int32 * len(columns))(*[c.kind for c in columns])
+        data = (C.c_void_p * len(columns))()
+        lexs = (C.POINTER(C.c_char_p) * len(columns))()
+        lsz = (C.c_int64 * len(columns))()
+        for i, c in enumerate(columns):
+            arr = np.ascontiguousarray(c.values, dtype=np.float64 if c.kind == FLOAT64 else np.int64)
+            keep.append(arr)
+            data[i] = arr.ctypes.data
+            if c.kind == STRING:
+                lx = (C.c_char_p * max(1, len(c.lexicon)))(*[s.encode() for s in c.lexicon])
+                keep.append(lx)
+                lexs[i] = C.cast(lx, C.POINTER(C.c_char_p))
+                lsz[i] = len(c.lexicon)
+        dist = None
+        if distinct is not None:
+            dist = (C.c_int64 * len(columns))(*distinct)
+        _check(self._lib.hawk_engine_put_columns(self._h, name.encode(), len(columns), names, kinds,
+                                                 n, data, lexs, lsz, dist, row_offset))
+
+    def generate(self, table: int, sf: float, seed: int = 42, row_begin: int = 0, rows: int = -1):
+        """Generates a synthetic table (include/hawk_gen.h) directly in HBM."""
+        _check(self._lib.hawk_engine_generate(self._h, table, sf, seed, row_begin, rows))
+
+    def drop(self, name: str):
+        _check(self._lib.hawk_engine_drop(self._h, name.encode()))
+
+    def table_rows(self, name: str) -> int:
+        return self._lib.hawk_engine_table_rows(self._h, name.encode())
+
+    def column_ptr(self, table: str, column: str) -> int:
+        return self._lib.hawk_engine_column(self._h, table.encode(), column.encode()) or 0
+
+    def flush_l2(self):
+        _check(self._lib.hawk_engine_flush_l2(self._h))
+
+    # ---- execution ----
+    def run(self, sql: str, config: str = "") -> Result:
+        r = C.c_void_p()
+        _check(self._lib.hawk_engine_run(self._h, sql.encode(), config.encode(), C.byref(r)))
+        try:
+            return _result_from(self._lib, r)
+        finally:
+            self._lib.hawk_result_free(r)
+
+    def run_partial(self, sql: str, config: str = "") -> tuple[np.ndarray, int, float]:
+        """Shard execution: (rows x width int64 partials, sink, kernel_ms)."""
+        p = C.c_void_p()
+        _check(self._lib.hawk_engine_run_partial(self._h, sql.encode(), config.encode(), C.byref(p)))
+        try:
+            rows = self._lib.hawk_partial_rows(p)
+            width = self._lib.hawk_partial_width(p)
+            n = rows * width
+            ptr = self._lib.hawk_partial_data(p)
+            data = (np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_int64)), shape=(n,)).copy()
+                    if n else np.zeros(0, np.int64))
+            return data.reshape(rows, width), self._lib.hawk_partial_sink(p), \
+                self._lib.hawk_partial_kernel_ms(p)
+        finally:
+            self._lib.hawk_partial_free(p)
+
+    def finalize(self, sql: str, parts: list[np.ndarray], config: str = "") -> Result:
+        arrs = [np.ascontiguousarray(p, dtype=np.int64) for p in parts]
+        data = (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+        rows = (C.c_int64 * len(arrs))(*[a.shape[0] if a.ndim == 2 else 1 for a in arrs])
+        r = C.c_void_p()
+        _check(self._lib.hawk_engine_finalize(self._h, sql.encode(), config.encode(), len(arrs),
+                                              data, rows, C.byref(r)))
+        try:
+            return _result_from(self._lib, r)
+        finally:
+            self._lib.hawk_result_free(r)
+
+    # ---- IR introspection ----
+    def pipeline_count(self, sql: str) -> int:
+        n = C.c_int32()
+        _check(self._lib.hawk_engine_pipeline_count(self._h, sql.encode(), C.byref(n)))
+        return n.value
+
+    def space_size(self, sql: str, pipeline: int) -> tuple[int, int]:
+        n, s = C.c_int32(), C.c_int32()
+        _check(self._lib.hawk_engine_space_size(self._h, sql.encode(), pipeline, C.byref(n),
+                                                C.byref(s)))
+        return n.value, s.value
+
+    def space_config(self, sql: str, pipeline: int, i: int) -> str:
+        buf = C.create_string_buffer(256)
+        _check(self._lib.hawk_engine_space_config(self._h, sql.encode(), pipeline, i, buf, 256))
+        return buf.value.decode()
+
+    def validate(self, sql: str, config: str = "") -> str:
+        buf = C.create_string_buffer(1 << 16)
+        _check(self._lib.hawk_engine_validate(self._h, sql.encode(), config.encode(), buf, 1 << 16))
+        return buf.value.decode()
+
+    def explain(self, sql: str, config: str = "") -> str:
+        buf = C.create_string_buffer(1 << 16)
+        _check(self._lib.hawk_engine_explain(self._h, sql.encode(), config.encode(), buf, 1 << 16))
+        return buf.value.decode()
+
+    # ---- optimizer ----
+    def measure(self, sqls: list[str], config: str, prune_ms: float = 1000.0, reps: int = 3) -> float:
+        arr = (C.c_char_p * len(sqls))(*[s.encode() for s in sqls])
+        ms = C.c_double()
+        _check(self._lib.hawk_engine_measure(self._h, arr, len(sqls), config.encode(), prune_ms,
+                                             reps, C.byref(ms)))
+        return ms.value
+
+    def learn(self, sqls: list[str], q: int = 3, prune_ms: float = 1000.0, reps: int = 3) -> dict:
+        arr = (C.c_char_p * len(sqls))(*[s.encode() for s in sqls])
+        buf = C.create_string_buffer(512)
+        ms, ev, sw = C.c_double(), C.c_int32(), C.c_int32()
+        _check(self._lib.hawk_engine_learn(self._h, arr, len(sqls), q, prune_ms, reps, buf, 512,
+                                           C.byref(ms), C.byref(ev), C.byref(sw)))
+        return dict(config=buf.value.decode(), ms=ms.value, evaluations=ev.value, sweeps=sw.value)
