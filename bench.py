@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-rows", type=int, default=4_000_000)
+    ap.add_argument("--prefetch", type=int, default=None, help="L2 bulk-prefetch distance (passes)")
     ap.add_argument("--sweep", nargs="*", default=None,
                     help="time each given config (or a built-in list) and print one line per config")
     return ap.parse_args()
@@ -58,6 +59,10 @@ def parse():
 
 SWEEP = [
     "single_pass/coalesced/branched;local_hash/coalesced/branched/linear_probing/murmur/wg=256/ht=1",
+    "single_pass/coalesced/branched;local_hash/coalesced/branched/linear_probing/murmur/wg=256/ht=4",
+    "single_pass/coalesced/branched;local_hash/coalesced/branched/linear_probing/murmur/wg=128/ht=8",
+    "single_pass/sequential/branched;local_hash/sequential/branched/linear_probing/murmur/wg=256/ht=4",
+    "single_pass/coalesced/branched;global_hash/coalesced/predicated/linear_probing/murmur/wg=256",
     "single_pass/coalesced/predicated;local_hash/coalesced/predicated/linear_probing/murmur/wg=256/ht=1",
     "single_pass/sequential/branched;local_hash/sequential/branched/linear_probing/murmur/wg=256/ht=1",
     "multi_pass/coalesced/branched/tm=1024;local_hash/coalesced/branched/linear_probing/murmur/wg=512/ht=1",
@@ -78,6 +83,9 @@ def run_sweep(args):
     query = args.query
     sf = args.sf or DEFAULT_SF[query]
     engine = Engine(0)
+    if args.prefetch is not None:
+        from paper_1709_00700_b200 import _native
+        _native.b200().hawk_b200_ctx_set_option(engine.ctx, b"prefetch_passes", args.prefetch)
     load_tables(engine, query, sf, args.seed, 0, 1)
     sql = Q.BENCH[query][0]
     for cfg in (args.sweep or SWEEP):

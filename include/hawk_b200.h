@@ -230,6 +230,8 @@ int32_t hawk_b200_ctx_sm_count(hawk_ctx* ctx, int32_t* sms);
 /* cudaStream_t of the context, as void* */
 void* hawk_b200_ctx_stream(hawk_ctx* ctx);
 int32_t hawk_b200_ctx_synchronize(hawk_ctx* ctx);
+/* Tuning knobs: "prefetch_passes" (COALESCED L2 bulk-prefetch distance, 0..16). */
+int32_t hawk_b200_ctx_set_option(hawk_ctx* ctx, const char* name, int64_t value);
 
 /* ---- device memory (HBM arena) ------------------------------------------- */
 int32_t hawk_b200_alloc(hawk_ctx* ctx, size_t bytes, void** d_ptr);
@@ -256,8 +258,9 @@ int32_t hawk_b200_gen_column_host(int32_t table, int32_t col, double sf, uint64_
 
 /* ---- hash-table runtime ---------------------------------- */
 /* eval_hash(function, x, seed/params) -> slot in [0, 2^log2_capacity)
- * (SPEC.md:399-407): murmur = fmix64(x ^ seed); multiply-shift =
- * ((seed|1) * x mod 2^64) >> (64 - log2_capacity). */
+ * (SPEC.md:399-407): murmur = fmix64(x ^ seed) masked; multiply-shift =
+ * (a * x mod 2^64) >> (64 - log2_capacity) with the odd per-seed multiplier
+ * a = (seed * 0x9e3779b97f4a7c15) | 1. */
 uint64_t hawk_b200_eval_hash(int32_t function, int64_t x, uint64_t seed, int32_t log2_capacity);
 /* Fills a join-table descriptor for `rows` build rows (capacity = next pow2
  * >= 2*rows) without allocating; *bytes = device bytes its slots need. The

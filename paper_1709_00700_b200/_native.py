@@ -54,6 +54,7 @@ def b200() -> C.CDLL:
         _sig(lib, "hawk_b200_ctx_sm_count", i32, vp, C.POINTER(i32))
         _sig(lib, "hawk_b200_ctx_stream", vp, vp)
         _sig(lib, "hawk_b200_ctx_synchronize", i32, vp)
+        _sig(lib, "hawk_b200_ctx_set_option", i32, vp, cp, i64)
         _sig(lib, "hawk_b200_alloc", i32, vp, C.c_size_t, C.POINTER(vp))
         _sig(lib, "hawk_b200_free", i32, vp, vp)
         _sig(lib, "hawk_b200_memcpy_h2d", i32, vp, vp, vp, C.c_size_t)

@@ -21,6 +21,8 @@ struct hawk_ctx {
   cudaStream_t stream = nullptr;
   int sms = 148;
   int smem_optin = 227 * 1024;
+  int prefetch_passes = 2;  // COALESCED: L2 bulk-prefetch distance in passes
+  int priv_groups = 8;      // HAGG_LOCAL: groups with thread-private accumulators
   int64_t l2_bytes = 0;
   // control block: [0] flags (int) [1] counter (unsigned) [2] cursor [3] total
   u64* d_ctrl = nullptr;
@@ -84,14 +86,17 @@ struct Launch {
   hk::LaunchShape shape;
 };
 
-void collect_staged(hk::KParams& kp, bool keys, bool aggs, bool project) {
+// Driver columns the role reads: prefetched into L2 ahead of each pass.
+void collect_prefetch(hk::KParams& kp, bool keys, bool aggs, bool project) {
   const hawk_pipeline& p = kp.p;
+  bool seen[HAWK_MAX_COLUMNS] = {};
+  kp.nprefetch = 0;
   std::memset(kp.stage_of, -1, sizeof kp.stage_of);
-  kp.nstaged = 0;
   auto add = [&](const hawk_operand& o) {
-    if (o.kind == HAWK_OPND_COLUMN && kp.stage_of[o.index] < 0) {
-      kp.stage_of[o.index] = (int8_t)kp.nstaged;
-      kp.staged_col[kp.nstaged++] = (int8_t)o.index;
+    if (o.kind == HAWK_OPND_COLUMN && !seen[o.index]) {
+      seen[o.index] = true;
+      kp.stage_of[o.index] = (int8_t)kp.nprefetch;
+      kp.prefetch_col[kp.nprefetch++] = (int8_t)o.index;
     }
   };
   for (int i = 0; i < p.nfilter; ++i) add(p.filter[i].lhs), add(p.filter[i].rhs);
@@ -107,16 +112,77 @@ void collect_staged(hk::KParams& kp, bool keys, bool aggs, bool project) {
     for (int i = 0; i < p.nproject; ++i) add(p.project[i]);
 }
 
-// Shared-memory layout [mbarriers | TMA stages | local table | scratch | state]
-// and tile size for one kernel role. Returns false when it cannot fit.
+bool same_operand(const hawk_operand& a, const hawk_operand& b) {
+  return a.kind == b.kind && a.type == b.type && a.index == b.index && a.probe == b.probe &&
+         a.bits == b.bits;
+}
+
+// FILTER compilation: an int64 comparison against a literal becomes a closed
+// range [lo, hi]; consecutive ranges on the same operand intersect. The
+// semantics are the oracle's (planner_reference.cpp:76-104): a conjunction.
+int compile_filters(const hawk_compare* in, int n, hk::KFilter* out) {
+  int m = 0;
+  for (int i = 0; i < n; ++i) {
+    const hawk_compare& c = in[i];
+    hk::KFilter f{};
+    f.lhs = c.lhs;
+    f.rhs = c.rhs;
+    f.op = c.op;
+    f.type = c.type;
+    const bool int_lit = c.type == HAWK_I64 && c.rhs.kind == HAWK_OPND_INT && c.lhs.type == HAWK_I64;
+    if (int_lit && c.op != HAWK_NE) {
+      const int64_t v = c.rhs.bits;
+      int64_t lo = INT64_MIN, hi = INT64_MAX;
+      bool empty = false;
+      switch (c.op) {
+        case HAWK_LT: empty = v == INT64_MIN; hi = v - (empty ? 0 : 1); break;
+        case HAWK_LE: hi = v; break;
+        case HAWK_EQ: lo = hi = v; break;
+        case HAWK_GE: lo = v; break;
+        case HAWK_GT: empty = v == INT64_MAX; lo = v + (empty ? 0 : 1); break;
+      }
+      if (!empty) {
+        if (m > 0 && out[m - 1].op == hk::kRange && same_operand(out[m - 1].lhs, c.lhs)) {
+          hk::KFilter& g = out[m - 1];
+          g.lo = std::max(g.lo, lo);
+          g.hi = std::min(g.hi, hi);
+          if (g.lo > g.hi) empty = true;
+          else continue;
+        } else {
+          f.op = hk::kRange;
+          f.lo = lo;
+          f.hi = hi;
+          out[m++] = f;
+          continue;
+        }
+      }
+      if (empty) {  // unsatisfiable: 0 = 1
+        f.op = HAWK_EQ;
+        f.type = HAWK_I64;
+        f.lhs = hawk_operand{HAWK_OPND_INT, HAWK_I64, 0, 0, 0};
+        f.rhs = hawk_operand{HAWK_OPND_INT, HAWK_I64, 0, 0, 1};
+        if (m > 0 && out[m - 1].op == hk::kRange && same_operand(out[m - 1].lhs, c.lhs)) --m;
+        out[m++] = f;
+        continue;
+      }
+    }
+    out[m++] = f;
+  }
+  return m;
+}
+
+// Shared-memory layout [local table | scratch | state] for one kernel role.
+// Returns false when it cannot fit.
 bool layout_smem(hawk_ctx* ctx, hk::KParams& kp, int role, int access, int impl, int unroll,
                  int block, size_t* smem_out) {
   const hawk_pipeline& p = kp.p;
-  const int R = access == HAWK_COALESCED ? unroll : 2 * unroll;
+  const int R = 4 * unroll;
+  (void)access;
   const bool agg = role == hk::K_AGG_LOCAL || role == hk::K_AGG_GLOBAL;
   const bool hagg = role == hk::K_HAGG_LOCAL || role == hk::K_HAGG_GLOBAL;
   kp.rid_base = p.narith * R;
-  kp.key_base = kp.rid_base + p.nprobe * R;
+  // HASH_AGGREGATE keeps its group-slot pointers in the row after the probe ids
+  kp.key_base = kp.rid_base + (p.nprobe + (hagg ? 1 : 0)) * R;
   kp.acc_base = kp.key_base + (hagg ? p.nkeys * R : 0);
   kp.state_words = kp.acc_base + (agg ? p.naggs : 0);
   const size_t state_bytes = (size_t)std::max(kp.state_words, 1) * block * 8;
@@ -132,28 +198,13 @@ bool layout_smem(hawk_ctx* ctx, hk::KParams& kp, int role, int access, int impl,
     kp.local_log2 = L;
     table_bytes = ((size_t)1 << L) * per_slot;
   }
-  const size_t scratch_bytes = 32 * HAWK_MAX_AGGS * 8;
-  size_t off = 128;
-  kp.smem_stage_off = (int)off;
-  size_t fixed = table_bytes + scratch_bytes + state_bytes + 3 * 128;
-  size_t stage_bytes = 0;
-  kp.tile_rows = 16;
-  kp.nstages = 1;
-  if (access == HAWK_COALESCED && kp.nstaged > 0) {
-    const size_t avail = (size_t)ctx->smem_optin > fixed + 128 ? ctx->smem_optin - fixed - 128 : 0;
-    const size_t target = std::min<size_t>(avail, block >= 512 ? 96 * 1024 : 48 * 1024);
-    int S = 3;
-    int64_t T = 4096;
-    while (T > 16 && (size_t)S * kp.nstaged * T * 8 > target) T >>= 1;
-    if ((size_t)S * kp.nstaged * T * 8 > target) {
-      S = 2;
-      if ((size_t)S * kp.nstaged * T * 8 > avail) return false;
-    }
-    kp.tile_rows = (int)T;
-    kp.nstages = S;
-    stage_bytes = (size_t)S * kp.nstaged * T * 8;
+  const size_t scratch_bytes = 33 * HAWK_MAX_AGGS * 8;
+  size_t off = 0;
+  kp.smem_stage_off = 0;
+  if (access == HAWK_COALESCED && kp.nprefetch > 0) {
+    // [mbarriers (128 B)][S pass tiles x C columns x B*R rows]
+    off = 128 + (size_t)kp.prefetch_passes * kp.nprefetch * block * R * 8;
   }
-  off += stage_bytes;
   off = (off + 127) & ~size_t(127);
   kp.smem_table_off = (int)off;
   off += table_bytes;
@@ -163,6 +214,25 @@ bool layout_smem(hawk_ctx* ctx, hk::KParams& kp, int role, int access, int impl,
   off = (off + 127) & ~size_t(127);
   kp.smem_state_off = (int)off;
   off += state_bytes;
+  kp.priv_groups = 0;
+  kp.smem_ord_off = kp.smem_priv_off = (int)off;
+  if (role == hk::K_HAGG_LOCAL && p.naggs > 0 && ctx->priv_groups > 0) {
+    // thread-private accumulators for the first GP groups of each CTA
+    const size_t per_group = (size_t)p.naggs * block * 8;
+    int gp = (int)std::min<size_t>((size_t)ctx->priv_groups, (48 * 1024) / per_group);
+    const int local_slots = (1 << kp.local_log2) * (impl == HAWK_CUCKOO ? 2 : 1);
+    const size_t need = ((off + 127) & ~size_t(127)) + (size_t)(local_slots + gp + 1) * 4 + 128 +
+                        (size_t)gp * per_group;
+    if (gp >= 1 && need <= (size_t)ctx->smem_optin) {
+      off = (off + 127) & ~size_t(127);
+      kp.smem_ord_off = (int)off;
+      off += (size_t)(local_slots + gp + 1) * 4;
+      off = (off + 127) & ~size_t(127);
+      kp.smem_priv_off = (int)off;
+      off += (size_t)gp * per_group;
+      kp.priv_groups = gp;
+    }
+  }
   if (off > (size_t)ctx->smem_optin) return false;
   *smem_out = off;
   return true;
@@ -204,10 +274,25 @@ int32_t prepare(hawk_ctx* ctx, const hawk_pipeline& pipe, const hawk_variant& v,
   const bool keys = role == hk::K_HAGG_LOCAL || role == hk::K_HAGG_GLOBAL || role == hk::K_PUT_SINGLE;
   const bool aggs = role <= hk::K_HAGG_GLOBAL;
   const bool project = role == hk::K_PROJECT_SINGLE || role == hk::K_PROJECT_SCATTER;
-  collect_staged(kp, keys, aggs, project);
+  kp.npre = compile_filters(pipe.filter, pipe.nfilter, kp.pre);
+  kp.npost = compile_filters(pipe.post, pipe.npost, kp.post);
+  collect_prefetch(kp, keys, aggs, project);
+  kp.prefetch_passes = std::max(1, std::min(ctx->prefetch_passes, 8));  // TMA stages
+  block = std::min(block, hk::kMaxBlock);
   size_t smem = 0;
-  if (!layout_smem(ctx, kp, role, v.memory_access, v.hash_table_impl, v.unroll_factor, block, &smem))
-    return HAWK_ERR_PLAN_TOO_LARGE;
+  // the TMA pipeline gets shallower before the plan is declared too large
+  // and finally the tile is read straight from HBM (coalesced, unstaged)
+  while (!layout_smem(ctx, kp, role, v.memory_access, v.hash_table_impl, v.unroll_factor, block,
+                      &smem)) {
+    if (v.memory_access == HAWK_COALESCED && kp.prefetch_passes > 1) {
+      --kp.prefetch_passes;
+    } else if (v.memory_access == HAWK_COALESCED && kp.nprefetch > 0) {
+      kp.nprefetch = 0;
+      std::memset(kp.stage_of, -1, sizeof kp.stage_of);
+    } else {
+      return HAWK_ERR_PLAN_TOO_LARGE;
+    }
+  }
   int64_t grid = grid_or_zero;
   if (grid <= 0) {  // persistent: fill every SM
     int ctas = 0;
@@ -218,7 +303,7 @@ int32_t prepare(hawk_ctx* ctx, const hawk_pipeline& pipe, const hawk_variant& v,
   }
   if (grid > 0x7fffffff) return HAWK_ERR_PLAN_TOO_LARGE;
   int64_t chunk = (pipe.nrows + grid - 1) / grid;
-  chunk = std::max<int64_t>(16, (chunk + 15) & ~int64_t(15));
+  chunk = std::max<int64_t>(64, (chunk + 63) & ~int64_t(63));
   kp.chunk_rows = chunk;
   shape.grid = dim3((unsigned)grid);
   shape.block = dim3((unsigned)block);
@@ -308,6 +393,19 @@ int32_t hawk_b200_ctx_sm_count(hawk_ctx* ctx, int32_t* sms) {
 }
 
 void* hawk_b200_ctx_stream(hawk_ctx* ctx) { return ctx->stream; }
+
+int32_t hawk_b200_ctx_set_option(hawk_ctx* ctx, const char* name, int64_t value) {
+  if (!ctx || !name) return HAWK_ERR_ARGUMENT;
+  if (std::strcmp(name, "prefetch_passes") == 0) {
+    ctx->prefetch_passes = (int)std::max<int64_t>(0, std::min<int64_t>(value, 16));
+    return HAWK_OK;
+  }
+  if (std::strcmp(name, "priv_groups") == 0) {
+    ctx->priv_groups = (int)std::max<int64_t>(0, std::min<int64_t>(value, 64));
+    return HAWK_OK;
+  }
+  return HAWK_ERR_ARGUMENT;
+}
 
 int32_t hawk_b200_ctx_synchronize(hawk_ctx* ctx) {
   HK_TRY(cudaStreamSynchronize(ctx->stream));
@@ -679,7 +777,11 @@ int32_t hawk_b200_run_pipeline(hawk_ctx* ctx, const hawk_pipeline* pipe, const h
                    : (local ? hk::K_AGG_LOCAL : hk::K_AGG_GLOBAL);
     // local: N = SMs x hash_table_count_multiplier tables, each served by a
     // work group of M = work_group_size threads
-    const int64_t grid = local ? (int64_t)ctx->sms * v->hash_table_count_multiplier : 0;
+    // (a work group wider than one 256-thread CTA spans wg/256 CTAs, each
+    // with its own slice of the group's table, merged like every local table)
+    const int64_t grid = local ? (int64_t)ctx->sms * v->hash_table_count_multiplier *
+                                     std::max(1, v->work_group_size / hk::kMaxBlock)
+                               : 0;
     st = prepare(ctx, p, *v, role, v->work_group_size, grid, 64, kp, shape);
     if (st != HAWK_OK) return st;
     if (grouped && (!p.sink_table.d_slots || p.sink_table.impl != v->hash_table_impl ||
@@ -701,7 +803,7 @@ int32_t hawk_b200_run_pipeline(hawk_ctx* ctx, const hawk_pipeline* pipe, const h
   } else if (s == HAWK_SINGLE_PASS) {
     // one worker (a 1024-thread CTA) per compute unit
     role = p.sink == HAWK_SINK_PROJECT ? hk::K_PROJECT_SINGLE : hk::K_PUT_SINGLE;
-    st = prepare(ctx, pe, *v, role, 1024, ctx->sms, 1, kp, shape);
+    st = prepare(ctx, pe, *v, role, hk::kMaxBlock, (int64_t)ctx->sms * 4, 1, kp, shape);
     if (st != HAWK_OK) return st;
     if (p.sink == HAWK_SINK_PROJECT) {
       out_stride = std::max<int64_t>(p.nrows, 1);

@@ -26,12 +26,19 @@ __host__ __device__ __forceinline__ u64 fmix64(u64 k) {
   return k;
 }
 
+// Per-seed odd multiplier of multiply-shift. The reference's descriptor seeds
+// are small integers (planner_pipelines.cpp:123), so they are spread over all
+// 64 bits first; a small multiplier would leave the high bits (the slot) empty.
+__host__ __device__ __forceinline__ u64 ms_multiplier(u64 seed) {
+  return (seed * 0x9e3779b97f4a7c15ull) | 1ull;
+}
+
 // slot in [0, 2^log2cap). Murmur: fmix64(x ^ seed) masked; multiply-shift:
-// (a*x mod 2^64) >> (64 - b) with a = seed | 1 (odd), b = log2cap >= 1.
+// (a*x mod 2^64) >> (64 - b) with a = ms_multiplier(seed) (odd), b = log2cap >= 1.
 template <int HFN>
 __host__ __device__ __forceinline__ u64 hash_slot(u64 x, u64 seed, int log2cap) {
   if (HFN == HAWK_MURMUR) return fmix64(x ^ seed) & ((1ull << log2cap) - 1ull);
-  return ((seed | 1ull) * x) >> (64 - log2cap);
+  return (ms_multiplier(seed) * x) >> (64 - log2cap);
 }
 
 __host__ __device__ __forceinline__ u64 hash_dispatch(int fn, u64 x, u64 seed, int log2cap) {
@@ -61,6 +68,18 @@ __device__ __forceinline__ void ldg128(const void* p, u64& a, u64& b) {
 }
 __device__ __forceinline__ u64 ld_volatile(const u64* p) {
   return *reinterpret_cast<const volatile u64*>(p);
+}
+// acquire loads: a published slot tag orders the claimer's key/accumulator
+// writes before our subsequent reads (generic addresses: smem or HBM)
+__device__ __forceinline__ u64 ld_acquire_cta(const u64* p) {
+  u64 v;
+  asm volatile("ld.acquire.cta.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ u64 ld_acquire_gpu(const u64* p) {
+  u64 v;
+  asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
 // ---- atomics on generic addresses (smem or HBM) -------------------------------
@@ -132,6 +151,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
       "r"(parity)
       : "memory");
+}
+// TMA bulk prefetch of a global range into L2 (bytes % 16 == 0, 16B aligned)
+__device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 // global -> shared bulk copy completing on `bar` (bytes % 16 == 0, 16B aligned)
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,

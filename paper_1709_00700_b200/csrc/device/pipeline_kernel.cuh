@@ -1,25 +1,26 @@
-// pipeline_kernel.cuh — the kernel template: LOOP driver (TMA-staged or
-// per-thread sequential), the per-row op chain, and the eight sink roles.
+// pipeline_kernel.cuh — the kernel template: LOOP driver (coalesced with L2
+// bulk prefetch, or per-thread sequential), the per-row op chain, and the
+// eight sink roles.
 #pragma once
 
-#include "pipeline.cuh"
+#include "tables.cuh"
 
 namespace hk {
 
-// FILTER -> HASH_PROBE -> FILTER -> ARITHMETIC over one row batch.
+// FILTER -> HASH_PROBE -> FILTER -> ARITHMETIC over one batch of R rows.
 template <int ACCESS, int PRED, int IMPL, int HFN, int R>
-__device__ __forceinline__ void evaluate(const KParams& kp, const Batch<R>& b,
-                                         const int64_t* stage, State<R>& s) {
+__device__ __forceinline__ void evaluate(const KParams& kp, const Batch<R, ACCESS>& b,
+                                         State<R>& s) {
   const hawk_pipeline& p = kp.p;
   s.alive = b.valid;
   // driver FILTER conjuncts (planner_reference.cpp:97-104)
-  for (int i = 0; i < p.nfilter; ++i) {
+  for (int i = 0; i < kp.npre; ++i) {
     if (PRED == HAWK_BRANCHED && s.alive == 0u) return;
-    const hawk_compare& c = p.filter[i];
+    const KFilter& f = kp.pre[i];
     u64 x[R], y[R];
-    fetch<ACCESS, PRED, R>(kp, c.lhs, c.type, b, s, stage, x);
-    fetch<ACCESS, PRED, R>(kp, c.rhs, c.type, b, s, stage, y);
-    s.alive &= compare_rows<R>(c.op, c.type, x, y);
+    fetch<PRED, R, ACCESS>(kp, f.lhs, f.type, b, s, x);
+    if (f.op != kRange) fetch<PRED, R, ACCESS>(kp, f.rhs, f.type, b, s, y);
+    s.alive &= compare_rows<R>(f, x, y);
   }
   // HASH_PROBE chain: branched opens a found-scope, predicated
   // folds the match bit into result_increment.
@@ -27,32 +28,36 @@ __device__ __forceinline__ void evaluate(const KParams& kp, const Batch<R>& b,
     if (PRED == HAWK_BRANCHED && s.alive == 0u) return;
     const hawk_probe& pr = p.probe[i];
     u64 k[R];
-    fetch<ACCESS, PRED, R>(kp, pr.key, HAWK_I64, b, s, stage, k);
+    fetch<PRED, R, ACCESS>(kp, pr.key, HAWK_I64, b, s, k);
     const hawk_table& t = p.tables[pr.table];
+    int32_t r[R];
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       const bool act = PRED == HAWK_PREDICATED ? ((b.valid >> j) & 1u) : ((s.alive >> j) & 1u);
-      const int32_t r = act ? table_find<IMPL, HFN>(t, k[j]) : -1;
-      if (r < 0) s.alive &= ~(1u << j);
-      s.rid(i, j) = (u64)(r < 0 ? 0 : r);
+      r[j] = act ? table_find<IMPL, HFN>(t, k[j]) : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      if (r[j] < 0) s.alive &= ~(1u << j);
+      s.rid(i, j) = (u64)(r[j] < 0 ? 0 : r[j]);
     }
   }
   // post-probe FILTER conjuncts (operands may be build payloads)
-  for (int i = 0; i < p.npost; ++i) {
+  for (int i = 0; i < kp.npost; ++i) {
     if (PRED == HAWK_BRANCHED && s.alive == 0u) return;
-    const hawk_compare& c = p.post[i];
+    const KFilter& f = kp.post[i];
     u64 x[R], y[R];
-    fetch<ACCESS, PRED, R>(kp, c.lhs, c.type, b, s, stage, x);
-    fetch<ACCESS, PRED, R>(kp, c.rhs, c.type, b, s, stage, y);
-    s.alive &= compare_rows<R>(c.op, c.type, x, y);
+    fetch<PRED, R, ACCESS>(kp, f.lhs, f.type, b, s, x);
+    if (f.op != kRange) fetch<PRED, R, ACCESS>(kp, f.rhs, f.type, b, s, y);
+    s.alive &= compare_rows<R>(f, x, y);
   }
   // ARITHMETIC into registers 0..narith-1
   for (int a = 0; a < p.narith; ++a) {
     if (PRED == HAWK_BRANCHED && s.alive == 0u) return;
     const hawk_arith& ar = p.arith[a];
     u64 x[R], y[R], z[R];
-    fetch<ACCESS, PRED, R>(kp, ar.lhs, ar.type, b, s, stage, x);
-    fetch<ACCESS, PRED, R>(kp, ar.rhs, ar.type, b, s, stage, y);
+    fetch<PRED, R, ACCESS>(kp, ar.lhs, ar.type, b, s, x);
+    fetch<PRED, R, ACCESS>(kp, ar.rhs, ar.type, b, s, y);
     arith_rows<R>(ar.op, ar.type, x, y, z);
 #pragma unroll
     for (int j = 0; j < R; ++j) s.reg(a, j) = z[j];
@@ -81,10 +86,11 @@ __device__ __forceinline__ u64 block_exclusive_scan(u64 v, u64* scratch, u64& to
   return excl;
 }
 
+
 template <int ROLE, int ACCESS, int PRED, int IMPL, int HFN, int U>
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(kMaxBlock, U == 1 ? 3 : (U == 2 ? 2 : 1))
     pipeline_kernel(const __grid_constant__ KParams kp) {
-  constexpr int R = ACCESS == HAWK_COALESCED ? U : 2 * U;
+  constexpr int R = 4 * U;
   extern __shared__ __align__(128) unsigned char smem[];
   const hawk_pipeline& p = kp.p;
   const int B = blockDim.x;
@@ -105,21 +111,40 @@ __global__ void __launch_bounds__(1024)
   if constexpr (ROLE == K_AGG_LOCAL || ROLE == K_AGG_GLOBAL) {
     for (int a = 0; a < p.naggs; ++a) s.acc(a) = agg_identity(p.aggs[a].fn, p.aggs[a].type);
   }
-  u64 count = 0;       // COUNT role
-  u64 running = 0;     // SCATTER role: rows written by this CTA so far
+  u64 count = 0;    // COUNT role
+  u64 running = 0;  // SCATTER role: rows written by this CTA so far
   u64* local_table = reinterpret_cast<u64*>(smem + kp.smem_table_off);
   const int K = p.nkeys;
   const int words = 1 + p.nkeys + p.naggs;
+  // HAGG_LOCAL: the first priv_groups groups a CTA meets get dense ordinals
+  // and thread-private accumulators (plain shared-memory read-modify-write,
+  // no atomics); the CTA folds them into its table at the end. Low-cardinality
+  // group-bys (TPC-H Q1: 4 groups) otherwise serialise on a few atomics.
+  const int GP = ROLE == K_HAGG_LOCAL ? kp.priv_groups : 0;
+  const int A = p.naggs;
+  const int local_slots = (1 << kp.local_log2) * (IMPL == HAWK_CUCKOO ? 2 : 1);
+  int* ordinal = reinterpret_cast<int*>(smem + kp.smem_ord_off);  // [local_slots]
+  int* ord_slot = ordinal + local_slots;                           // [GP]
+  int* nord = ord_slot + GP;                                       // [1]
+  u64* priv = reinterpret_cast<u64*>(smem + kp.smem_priv_off);
   if constexpr (ROLE == K_HAGG_LOCAL) {
-    const int slots = (1 << kp.local_log2) * (IMPL == HAWK_CUCKOO ? 2 : 1);
-    for (int i = threadIdx.x; i < slots; i += B) local_table[(size_t)i * words] = 0ull;
+    for (int i = threadIdx.x; i < local_slots; i += B) local_table[(size_t)i * words] = 0ull;
+    if (GP > 0) {
+      for (int i = threadIdx.x; i < local_slots; i += B) ordinal[i] = -1;
+      for (int i = threadIdx.x; i < GP; i += B) ord_slot[i] = -1;
+      if (threadIdx.x == 0) *nord = 0;
+      for (int w = 0; w < GP * A; ++w)
+        priv[(size_t)w * B + threadIdx.x] = agg_identity(p.aggs[w % A].fn, p.aggs[w % A].type);
+    }
     __syncthreads();
   }
   u64 scatter_base = 0;
   if constexpr (ROLE == K_PROJECT_SCATTER) scatter_base = (u64)kp.d_offsets[blockIdx.x];
+  u64 last_key[HAWK_MAX_KEYS] = {0, 0, 0, 0};  // HAGG: the thread's last group
+  u64 last_target = 0;
 
-  auto process = [&](const Batch<R>& b, const int64_t* stage) {
-    evaluate<ACCESS, PRED, IMPL, HFN, R>(kp, b, stage, s);
+  auto process = [&](const Batch<R, ACCESS>& b) {
+    evaluate<ACCESS, PRED, IMPL, HFN, R>(kp, b, s);
     const uint32_t alive = s.alive;
     if constexpr (ROLE == K_AGG_LOCAL || ROLE == K_AGG_GLOBAL) {
       // AGGREGATE: predicated SUM/COUNT multiply by the
@@ -133,7 +158,7 @@ __global__ void __launch_bounds__(1024)
           continue;
         }
         u64 v[R];
-        fetch<ACCESS, PRED, R>(kp, g.input, g.type, b, s, stage, v);
+        fetch<PRED, R, ACCESS>(kp, g.input, g.type, b, s, v);
         if (g.fn == HAWK_SUM && g.type == HAWK_I64) {
           u64 sum = 0;
 #pragma unroll
@@ -154,34 +179,108 @@ __global__ void __launch_bounds__(1024)
       if (PRED == HAWK_BRANCHED && alive == 0u) return;
       for (int i = 0; i < K; ++i) {
         u64 v[R];
-        fetch<ACCESS, PRED, R>(kp, p.keys[i], HAWK_I64, b, s, stage, v);
+        fetch<PRED, R, ACCESS>(kp, p.keys[i], HAWK_I64, b, s, v);
 #pragma unroll
         for (int j = 0; j < R; ++j) s.key(i, j) = v[j];
       }
-      u64* slot[R];
+      // find or claim each alive row's group; slot pointers go to the
+      // per-thread state (rows are not unrolled here: the probe sequence is
+      // data dependent and inlining it R times would only add registers)
       const hawk_table& gt = p.sink_table;
       const int kstride = R * B;
+#pragma unroll 1
+      for (int j = 0; j < R; ++j) {
+        u64 target = 0;  // slot pointer (even), (ordinal << 1) | 1 (private), 0 (none)
+        if ((alive >> j) & 1u) {
+          const u64* kj = &s.key(0, j);
+          // consecutive rows of one group skip the table lookup
+          bool same = last_target != 0;
+#pragma unroll
+          for (int i = 0; i < HAWK_MAX_KEYS; ++i)
+            if (i < K) same &= kj[(size_t)i * kstride] == last_key[i];
+          if (same) {
+            s.rid(p.nprobe, j) = last_target;
+            continue;
+          }
+          u64* slot = nullptr;
+          if constexpr (ROLE == K_HAGG_LOCAL) {
+            int si = 0;
+            slot = agg_find_or_insert<IMPL, HFN, true>(kp, local_table, kp.local_log2, gt.seed,
+                                                      kj, kstride, nullptr, &si);
+            if (slot != nullptr && GP > 0) {
+              // dense ordinals: exactly one thread per group (the one that
+              // moves the slot from -1 to -2) draws the next ordinal
+              volatile int* ov = reinterpret_cast<volatile int*>(ordinal + si);
+              int o = *ov;
+              if (o < 0) {
+                if (o == -1 && atomicCAS(ordinal + si, -1, -2) == -1) {
+                  const int mine = atomicAdd(nord, 1);
+                  o = mine < GP ? mine : GP;
+                  if (o < GP) ord_slot[o] = si;
+                  __threadfence_block();
+                  *ov = o;
+                } else {
+                  while ((o = *ov) < 0) {
+                  }
+                }
+              }
+              if (o < GP) target = ((u64)o << 1) | 1ull;
+            }
+          }
+          if (target == 0 && slot == nullptr)
+            slot = agg_find_or_insert<IMPL, HFN, false>(
+                kp, reinterpret_cast<u64*>(gt.d_slots), gt.log2_capacity, gt.seed, kj, kstride,
+                kp.d_cursor);
+          if (target == 0) {
+            if (slot == nullptr) atomicOr(kp.d_flags, HAWK_FLAG_TABLE_FULL);
+            target = reinterpret_cast<u64>(slot);
+          }
+#pragma unroll
+          for (int i = 0; i < HAWK_MAX_KEYS; ++i)
+            if (i < K) last_key[i] = kj[(size_t)i * kstride];
+          last_target = target;
+        }
+        s.rid(p.nprobe, j) = target;  // the row after the probe ids
+      }
+      // targets of the R rows: private word offset ((ord*A*B + t) << 1 | 1),
+      // a slot pointer, or 0; loaded once for all aggregates
+      u64 tw[R];
 #pragma unroll
       for (int j = 0; j < R; ++j) {
-        slot[j] = nullptr;
-        if (!((alive >> j) & 1u)) continue;
-        const u64* kj = &s.key(0, j);
-        if constexpr (ROLE == K_HAGG_LOCAL)
-          slot[j] = agg_find_or_insert<IMPL, HFN, true>(kp, local_table, kp.local_log2, gt.seed,
-                                                       kj, kstride, nullptr);
-        if (slot[j] == nullptr)
-          slot[j] = agg_find_or_insert<IMPL, HFN, false>(
-              kp, reinterpret_cast<u64*>(gt.d_slots), gt.log2_capacity, gt.seed, kj, kstride,
-              kp.d_cursor);
-        if (slot[j] == nullptr) atomicOr(kp.d_flags, HAWK_FLAG_TABLE_FULL);
+        const u64 t = s.rid(p.nprobe, j);
+        tw[j] = (t & 1ull) ? ((((t >> 1) * (u64)A * (u64)B + threadIdx.x) << 1) | 1ull) : t;
       }
-      for (int a = 0; a < p.naggs; ++a) {
+      for (int a = 0; a < A; ++a) {
         const hawk_agg& g = p.aggs[a];
-        u64 v[R];
-        if (g.fn != HAWK_COUNT) fetch<ACCESS, PRED, R>(kp, g.input, g.type, b, s, stage, v);
+        u64* pa = priv + (size_t)a * B;
+        const int agg_word = 1 + K + a;
+        if (g.fn == HAWK_COUNT || (g.fn == HAWK_SUM && g.type == HAWK_I64)) {
+          // the hot case (TPC-H Q1: 5 SUMs + 1 COUNT): add, no dispatch per row
+          u64 v[R];
+          if (g.fn == HAWK_COUNT) {
 #pragma unroll
-        for (int j = 0; j < R; ++j)
-          if (slot[j]) agg_update(slot[j] + 1 + K + a, g.fn, g.type, g.fn == HAWK_COUNT ? 1ull : v[j]);
+            for (int j = 0; j < R; ++j) v[j] = 1ull;
+          } else {
+            fetch<PRED, R, ACCESS>(kp, g.input, g.type, b, s, v);
+          }
+#pragma unroll
+          for (int j = 0; j < R; ++j) {
+            if (tw[j] & 1ull) pa[tw[j] >> 1] += v[j];
+            else if (tw[j]) atomic_add_i(reinterpret_cast<u64*>(tw[j]) + agg_word, v[j]);
+          }
+        } else {
+          u64 v[R];
+          fetch<PRED, R, ACCESS>(kp, g.input, g.type, b, s, v);
+#pragma unroll
+          for (int j = 0; j < R; ++j) {
+            if (tw[j] & 1ull) {
+              u64& acc = pa[tw[j] >> 1];
+              acc = agg_combine(g.fn, g.type, acc, v[j]);
+            } else if (tw[j]) {
+              agg_update(reinterpret_cast<u64*>(tw[j]) + agg_word, g.fn, g.type, v[j]);
+            }
+          }
+        }
       }
     } else if constexpr (ROLE == K_PROJECT_SINGLE) {
       // single pass: warp-aggregated atomic output cursor
@@ -197,7 +296,7 @@ __global__ void __launch_bounds__(1024)
         const u64 pos = base + incl - cnt;
         for (int i = 0; i < p.nproject; ++i) {
           u64 v[R];
-          fetch<ACCESS, PRED, R>(kp, p.project[i], p.project[i].type, b, s, stage, v);
+          fetch<PRED, R, ACCESS>(kp, p.project[i], p.project[i].type, b, s, v);
           int64_t* out = kp.d_out + (size_t)i * kp.out_stride + pos;
           int k = 0;
 #pragma unroll
@@ -215,7 +314,7 @@ __global__ void __launch_bounds__(1024)
         const u64 pos = scatter_base + running + excl;
         for (int i = 0; i < p.nproject; ++i) {
           u64 v[R];
-          fetch<ACCESS, PRED, R>(kp, p.project[i], p.project[i].type, b, s, stage, v);
+          fetch<PRED, R, ACCESS>(kp, p.project[i], p.project[i].type, b, s, v);
           int64_t* out = kp.d_out + (size_t)i * kp.out_stride + pos;
           int k = 0;
 #pragma unroll
@@ -227,84 +326,75 @@ __global__ void __launch_bounds__(1024)
     } else if constexpr (ROLE == K_PUT_SINGLE) {
       if (PRED == HAWK_BRANCHED && alive == 0u) return;
       u64 key[R];
-      fetch<ACCESS, PRED, R>(kp, p.keys[0], HAWK_I64, b, s, stage, key);
+      fetch<PRED, R, ACCESS>(kp, p.keys[0], HAWK_I64, b, s, key);
 #pragma unroll
       for (int j = 0; j < R; ++j)
         if ((alive >> j) & 1u)
-          table_insert<IMPL, HFN>(p.sink_table, key[j], (u64)(b.row[j] + p.row_offset),
+          table_insert<IMPL, HFN>(p.sink_table, key[j], (u64)(b.row(j) + p.row_offset),
                                   kp.d_flags);
     }
   };
 
   // ---- LOOP ----
+  const int64_t len = ce - cb;
   if constexpr (ACCESS == HAWK_COALESCED) {
-    // CTA-contiguous tiles; every referenced driver column of a tile is staged
-    // into shared memory with one TMA bulk copy, nstages deep.
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
-    int64_t* stages = reinterpret_cast<int64_t*>(smem + kp.smem_stage_off);
-    const int T = kp.tile_rows, S = kp.nstages, C = kp.nstaged;
-    const int64_t ntiles = ce > cb ? (ce - cb + T - 1) / T : 0;
-    if (threadIdx.x == 0) {
+    // Pass tiles of B*R rows: every referenced driver column of a tile is
+    // staged into shared memory by one TMA bulk copy (cp.async.bulk), S tiles
+    // in flight; thread t consumes tile rows t + jB.
+    const int64_t pass_rows = (int64_t)B * R;
+    const int64_t npasses = (len + pass_rows - 1) / pass_rows;
+    const int S = kp.prefetch_passes, C = kp.nprefetch;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kp.smem_stage_off);
+    int64_t* stages = reinterpret_cast<int64_t*>(smem + kp.smem_stage_off + 128);
+    if (threadIdx.x == 0 && C > 0) {
       for (int i = 0; i < S; ++i) mbar_init(&bars[i], 1);
       fence_mbar_init();
     }
     __syncthreads();
-    auto issue = [&](int64_t tile) {
-      const int st = (int)(tile % S);
-      const int64_t tb = cb + tile * T;
-      const int64_t rows = min((int64_t)T, ce - tb);
+    auto issue = [&](int64_t ps) {
+      const int st = (int)(ps % S);
+      const int64_t b0 = cb + ps * pass_rows;
+      const int64_t rows = min(pass_rows, ce - b0);
       const uint32_t bytes = (uint32_t)(((rows + 1) & ~1ll) * 8);
       mbar_arrive_expect_tx(&bars[st], bytes * (uint32_t)C);
       for (int c = 0; c < C; ++c)
-        tma_load_1d(stages + ((size_t)st * C + c) * T,
-                    reinterpret_cast<const int64_t*>(p.d_columns[kp.staged_col[c]]) + tb, bytes,
+        tma_load_1d(stages + ((size_t)st * C + c) * pass_rows,
+                    reinterpret_cast<const int64_t*>(p.d_columns[kp.prefetch_col[c]]) + b0, bytes,
                     &bars[st]);
     };
     if (threadIdx.x == 0 && C > 0)
-      for (int64_t t = 0; t < min((int64_t)S, ntiles); ++t) issue(t);
-    const int per_thread = (T + B - 1) / B;
-    for (int64_t tile = 0; tile < ntiles; ++tile) {
-      const int st = (int)(tile % S);
-      if (C > 0) mbar_wait(&bars[st], (uint32_t)((tile / S) & 1));
-      const int64_t* stage = stages + (size_t)st * C * T;
-      const int64_t tb = cb + tile * T;
-      const int rows = (int)min((int64_t)T, ce - tb);
-      for (int k = 0; k < per_thread; k += U) {
-        Batch<R> b;
-        b.valid = 0;
+      for (int64_t ps = 0; ps < min((int64_t)S, npasses); ++ps) issue(ps);
+    for (int64_t ps = 0; ps < npasses; ++ps) {
+      const int st = (int)(ps % S);
+      if (C > 0) mbar_wait(&bars[st], (uint32_t)((ps / S) & 1));
+      Batch<R, ACCESS> b;
+      b.base = cb + ps * pass_rows;
+      b.B = B;
+      b.stage = C > 0 ? stages + (size_t)st * C * pass_rows : nullptr;
+      b.valid = 0;
 #pragma unroll
-        for (int j = 0; j < R; ++j) {
-          const int r = threadIdx.x + (k + j) * B;
-          const bool ok = (k + j) < per_thread && r < rows;
-          b.valid |= (uint32_t)ok << j;
-          b.sidx[j] = ok ? r : 0;
-          b.row[j] = tb + (ok ? r : 0);
-        }
-        process(b, stage);
-      }
-      __syncthreads();
-      if (threadIdx.x == 0 && C > 0 && tile + S < ntiles) {
+      for (int j = 0; j < R; ++j) b.valid |= (uint32_t)(b.row(j) < ce) << j;
+      process(b);
+      __syncthreads();  // every thread is done with stage st
+      if (threadIdx.x == 0 && C > 0 && ps + S < npasses) {
         fence_proxy_async();
-        issue(tile + S);
+        issue(ps + S);
       }
     }
   } else {
     // each thread scans its own contiguous sub-chunk with 128-bit loads
-    const int64_t len = ce - cb;
-    const int64_t per = (((len + B - 1) / B) + 1) & ~1ll;
+    const int64_t per = ((((len + B - 1) / B) + R - 1) / R) * R;
     const int64_t ts = cb + (int64_t)threadIdx.x * per;
     const int64_t te = min(ce, ts + per);
     for (int64_t k = 0; k < per; k += R) {
-      Batch<R> b;
+      Batch<R, ACCESS> b;
+      b.base = ts + k;
+      b.B = B;
+      b.stage = nullptr;
       b.valid = 0;
 #pragma unroll
-      for (int j = 0; j < R; ++j) {
-        const int64_t r = ts + k + j;
-        b.valid |= (uint32_t)(r < te) << j;
-        b.row[j] = r < te ? r : 0;
-        b.sidx[j] = 0;
-      }
-      process(b, nullptr);
+      for (int j = 0; j < R; ++j) b.valid |= (uint32_t)(ts + k + j < te) << j;
+      process(b);
     }
   }
 
@@ -361,8 +451,33 @@ __global__ void __launch_bounds__(1024)
     // HostMergeHashTables on the device: fold the CTA's smem partials into
     // the global table with atomics.
     __syncthreads();
+    if (GP > 0) {
+      // fold the thread-private accumulators of every ordinal group into its
+      // slot: one warp per (group, aggregate) pair, fixed order
+      const int n = min(*nord, GP);
+      const int lane = lane_id(), warp = threadIdx.x >> 5, nwarps = (B + 31) >> 5;
+      const unsigned mask = warp_mask();
+      const int wsize = warp_size_here();
+      for (int pa = warp; pa < n * A; pa += nwarps) {
+        const int o = pa / A, a = pa % A;
+        if (ord_slot[o] < 0) continue;  // ordinal lost a claim race: never used
+        const int fn = p.aggs[a].fn == HAWK_COUNT ? HAWK_SUM : p.aggs[a].fn;
+        const int ty = p.aggs[a].type;
+        u64 v = agg_identity(fn, ty);
+        for (int t = lane; t < B; t += 32) v = agg_combine(fn, ty, v, priv[(size_t)pa * B + t]);
+        for (int off = 16; off > 0; off >>= 1) {
+          u64 w = __shfl_down_sync(mask, v, off);
+          if (lane + off < wsize) v = agg_combine(fn, ty, v, w);
+        }
+        if (lane == 0) {
+          u64* acc = local_table + (size_t)ord_slot[o] * words + 1 + K + a;
+          *acc = agg_combine(fn, ty, *acc, v);
+        }
+      }
+      __syncthreads();
+    }
     const hawk_table& gt = p.sink_table;
-    const int slots = (1 << kp.local_log2) * (IMPL == HAWK_CUCKOO ? 2 : 1);
+    const int slots = local_slots;
     for (int i = threadIdx.x; i < slots; i += B) {
       const u64* sl = local_table + (size_t)i * words;
       if (sl[0] == 0ull) continue;
