@@ -51,7 +51,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-rows", type=int, default=4_000_000)
-    ap.add_argument("--prefetch", type=int, default=None, help="L2 bulk-prefetch distance (passes)")
+    ap.add_argument("--prefetch", type=int, default=None, help="TMA pipeline depth (pass tiles)")
+    ap.add_argument("--stage", type=int, default=1, help="1: TMA-staged pass tiles (coalesced)")
+    ap.add_argument("--jit", type=int, default=1,
+                    help="1: compiled programs (NVRTC), 0: the AOT interpreter instantiations")
     ap.add_argument("--sweep", nargs="*", default=None,
                     help="time each given config (or a built-in list) and print one line per config")
     return ap.parse_args()
@@ -84,8 +87,9 @@ def run_sweep(args):
     sf = args.sf or DEFAULT_SF[query]
     engine = Engine(0)
     if args.prefetch is not None:
-        from paper_1709_00700_b200 import _native
-        _native.b200().hawk_b200_ctx_set_option(engine.ctx, b"prefetch_passes", args.prefetch)
+        engine.set_option("prefetch_passes", args.prefetch)
+    engine.set_option("jit", args.jit)
+    engine.set_option("stage", args.stage)
     load_tables(engine, query, sf, args.seed, 0, 1)
     sql = Q.BENCH[query][0]
     for cfg in (args.sweep or SWEEP):
@@ -302,6 +306,8 @@ def main():
     cfg = args.config or DEFAULT_CONFIG[query]
     sql = Q.BENCH[query][0]
     engine = Engine(local)
+    engine.set_option("jit", args.jit)
+    engine.set_option("stage", args.stage)
     per_rank = load_tables(engine, query, sf, args.seed, rank, world)
     lib = _native.b200()
     stream = torch.cuda.ExternalStream(lib.hawk_b200_ctx_stream(engine.ctx), device=torch.device("cuda", local))

@@ -19,8 +19,19 @@
 #ifndef HAWK_B200_H
 #define HAWK_B200_H
 
+#ifdef __CUDACC_RTC__ /* runtime-compiled programs (jit.cu): fixed-width types only */
+typedef signed char int8_t;
+typedef short int16_t;
+typedef int int32_t;
+typedef long long int64_t;
+typedef unsigned char uint8_t;
+typedef unsigned short uint16_t;
+typedef unsigned int uint32_t;
+typedef unsigned long long uint64_t;
+#else
 #include <stddef.h>
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -219,6 +230,7 @@ enum {
 
 typedef struct hawk_ctx hawk_ctx;
 
+#ifndef __CUDACC_RTC__ /* the entry points are host code */
 /* ---- context ------------------------------------------------------------ */
 const char* hawk_b200_version(void);
 const char* hawk_b200_status_string(int32_t status);
@@ -230,8 +242,20 @@ int32_t hawk_b200_ctx_sm_count(hawk_ctx* ctx, int32_t* sms);
 /* cudaStream_t of the context, as void* */
 void* hawk_b200_ctx_stream(hawk_ctx* ctx);
 int32_t hawk_b200_ctx_synchronize(hawk_ctx* ctx);
-/* Tuning knobs: "prefetch_passes" (COALESCED L2 bulk-prefetch distance, 0..16). */
+/* Knobs: "jit" (1 = compiled programs, 0 = the AOT interpreter instantiations),
+ * "prefetch_passes" (COALESCED TMA pipeline depth, 1..8), "priv_groups"
+ * (HASH_AGGREGATE local: groups with thread-private accumulators). */
 int32_t hawk_b200_ctx_set_option(hawk_ctx* ctx, const char* name, int64_t value);
+
+/* ---- compiled programs (the paper's code generation, §7) --------- */
+/* The CUDA source generated for a lowered pipeline under a variant: the
+ * hand-written kernel skeleton instantiated with a program policy whose ops
+ * are straight-line code (compiled with NVRTC for sm_100a when "jit" is on). */
+int32_t hawk_b200_program_source(const hawk_pipeline* pipeline, const hawk_variant* variant,
+                                 char* buf, int32_t len);
+/* Compiles it (NVRTC only, no GPU needed); log receives compiler errors. */
+int32_t hawk_b200_program_compile(const hawk_pipeline* pipeline, const hawk_variant* variant,
+                                  char* log, int32_t len, size_t* cubin_bytes);
 
 /* ---- device memory (HBM arena) ------------------------------------------- */
 int32_t hawk_b200_alloc(hawk_ctx* ctx, size_t bytes, void** d_ptr);
@@ -309,6 +333,7 @@ int32_t hawk_b200_agg_table_extract(hawk_ctx* ctx, const hawk_pipeline* pipeline
  * (multi-GPU merge after an all-gather). */
 int32_t hawk_b200_agg_table_merge_rows(hawk_ctx* ctx, const hawk_pipeline* pipeline,
                                        hawk_table* table, const int64_t* d_rows, int64_t nrows);
+#endif /* !__CUDACC_RTC__ */
 
 #ifdef __cplusplus
 }

@@ -94,6 +94,9 @@ int32_t hawk_engine_space_config(hawk_engine* e, const char* sql, int32_t pipeli
 int32_t hawk_engine_validate(hawk_engine* e, const char* sql, const char* config, char* buf,
                              int32_t len);
 
+/* generates and NVRTC-compiles every pipeline's program (no GPU needed) */
+int32_t hawk_engine_compile_check(hawk_engine* e, const char* sql, const char* config, char* buf,
+                                  int32_t len);
 /* lowered device programs of every pipeline, one op per line */
 int32_t hawk_engine_explain(hawk_engine* e, const char* sql, const char* config, char* buf,
                             int32_t len);

@@ -132,6 +132,7 @@ def engine() -> C.CDLL:
         _sig(lib, "hawk_engine_space_config", i32, vp, cp, i32, i32, cp, i32)
         _sig(lib, "hawk_engine_validate", i32, vp, cp, cp, cp, i32)
         _sig(lib, "hawk_engine_explain", i32, vp, cp, cp, cp, i32)
+        _sig(lib, "hawk_engine_compile_check", i32, vp, cp, cp, cp, i32)
         _sig(lib, "hawk_engine_measure", i32, vp, C.POINTER(cp), i32, cp, f64, i32,
              C.POINTER(f64))
         _sig(lib, "hawk_engine_learn", i32, vp, C.POINTER(cp), i32, i32, f64, i32, cp, i32,

@@ -12,6 +12,7 @@
 #include "hawk_b200.h"
 #include "hawk_gen.h"
 #include "kernels_misc.cuh"
+#include "jit.cuh"
 #include "launch.cuh"
 
 using hk::u64;
@@ -22,7 +23,9 @@ struct hawk_ctx {
   int sms = 148;
   int smem_optin = 227 * 1024;
   int prefetch_passes = 2;  // COALESCED: L2 bulk-prefetch distance in passes
-  int priv_groups = 8;      // HAGG_LOCAL: groups with thread-private accumulators
+  int priv_groups = 64;     // HAGG_LOCAL: groups with thread-private accumulators
+  int jit = 0;              // compiled programs (jit.cu) instead of the interpreter
+  int stage = 1;            // COALESCED: stage pass tiles in smem with TMA
   int64_t l2_bytes = 0;
   // control block: [0] flags (int) [1] counter (unsigned) [2] cursor [3] total
   u64* d_ctrl = nullptr;
@@ -174,16 +177,18 @@ int compile_filters(const hawk_compare* in, int n, hk::KFilter* out) {
 // Shared-memory layout [local table | scratch | state] for one kernel role.
 // Returns false when it cannot fit.
 bool layout_smem(hawk_ctx* ctx, hk::KParams& kp, int role, int access, int impl, int unroll,
-                 int block, size_t* smem_out) {
+                 int block, size_t* smem_out, bool kp_jit) {
   const hawk_pipeline& p = kp.p;
   const int R = 4 * unroll;
   (void)access;
   const bool agg = role == hk::K_AGG_LOCAL || role == hk::K_AGG_GLOBAL;
   const bool hagg = role == hk::K_HAGG_LOCAL || role == hk::K_HAGG_GLOBAL;
-  kp.rid_base = p.narith * R;
+  // compiled programs keep ARITHMETIC registers and probe row ids in registers
+  kp.rid_base = kp_jit ? 0 : p.narith * R;
   // HASH_AGGREGATE keeps its group-slot pointers in the row after the probe ids
   kp.key_base = kp.rid_base + (p.nprobe + (hagg ? 1 : 0)) * R;
   kp.acc_base = kp.key_base + (hagg ? p.nkeys * R : 0);
+  if (kp_jit) kp.rid_base = kp.key_base = kp.acc_base = 0;  // keys/targets in registers
   kp.state_words = kp.acc_base + (agg ? p.naggs : 0);
   const size_t state_bytes = (size_t)std::max(kp.state_words, 1) * block * 8;
   const int words = 1 + p.nkeys + p.naggs;
@@ -243,6 +248,7 @@ int32_t launch(hawk_ctx* ctx, int role, const hawk_variant& v, const hk::KParams
   const int a = v.memory_access, pr = v.predication, im = v.hash_table_impl,
             hf = v.hash_function, u = v.unroll_factor;
   using namespace hk;
+  if (s.jit_fn) return hk::jit_launch(s.jit_fn, kp, s.grid, s.block, s.smem, ctx->stream);
   cudaError_t e = cudaErrorInvalidValue;
   switch (role * 2 + (a == HAWK_COALESCED ? 1 : 0)) {
 #define HK_CASE(NAME, ROLE, A) \
@@ -278,12 +284,25 @@ int32_t prepare(hawk_ctx* ctx, const hawk_pipeline& pipe, const hawk_variant& v,
   kp.npost = compile_filters(pipe.post, pipe.npost, kp.post);
   collect_prefetch(kp, keys, aggs, project);
   kp.prefetch_passes = std::max(1, std::min(ctx->prefetch_passes, 8));  // TMA stages
+  if (!ctx->stage) {  // coalesced loads straight from HBM, no TMA staging
+    kp.nprefetch = 0;
+    std::memset(kp.stage_of, -1, sizeof kp.stage_of);
+  }
   block = std::min(block, hk::kMaxBlock);
+  shape.jit_fn = nullptr;
+  if (ctx->jit) {  // compiled program: generate + NVRTC (cached), see jit.cu
+    std::string err;
+    const int32_t st = hk::jit_function(kp, role, v, &shape.jit_fn, &err);
+    if (st != HAWK_OK) {
+      fprintf(stderr, "hawk_b200: program compilation failed: %s\n", err.c_str());
+      return st;
+    }
+  }
   size_t smem = 0;
   // the TMA pipeline gets shallower before the plan is declared too large
   // and finally the tile is read straight from HBM (coalesced, unstaged)
   while (!layout_smem(ctx, kp, role, v.memory_access, v.hash_table_impl, v.unroll_factor, block,
-                      &smem)) {
+                      &smem, shape.jit_fn != nullptr)) {
     if (v.memory_access == HAWK_COALESCED && kp.prefetch_passes > 1) {
       --kp.prefetch_passes;
     } else if (v.memory_access == HAWK_COALESCED && kp.nprefetch > 0) {
@@ -296,7 +315,8 @@ int32_t prepare(hawk_ctx* ctx, const hawk_pipeline& pipe, const hawk_variant& v,
   int64_t grid = grid_or_zero;
   if (grid <= 0) {  // persistent: fill every SM
     int ctas = 0;
-    int32_t st = occupancy(role, v, block, smem, &ctas);
+    int32_t st = shape.jit_fn ? hk::jit_occupancy(shape.jit_fn, block, smem, &ctas)
+                              : occupancy(role, v, block, smem, &ctas);
     if (st != HAWK_OK) return st;
     if (ctas < 1) return HAWK_ERR_PLAN_TOO_LARGE;
     grid = (int64_t)ctx->sms * std::min<int64_t>(ctas, per_sm_cap);
@@ -394,10 +414,62 @@ int32_t hawk_b200_ctx_sm_count(hawk_ctx* ctx, int32_t* sms) {
 
 void* hawk_b200_ctx_stream(hawk_ctx* ctx) { return ctx->stream; }
 
+static int main_role(const hawk_pipeline& p, const hawk_variant& v) {
+  const bool local = v.strategy == HAWK_LOCAL_HASH, single = v.strategy == HAWK_SINGLE_PASS;
+  switch (p.sink) {
+    case HAWK_SINK_AGGREGATE: return local ? hk::K_AGG_LOCAL : hk::K_AGG_GLOBAL;
+    case HAWK_SINK_HASH_AGGREGATE: return local ? hk::K_HAGG_LOCAL : hk::K_HAGG_GLOBAL;
+    case HAWK_SINK_PROJECT: return single ? hk::K_PROJECT_SINGLE : hk::K_PROJECT_SCATTER;
+    default: return single ? hk::K_PUT_SINGLE : hk::K_PROJECT_SCATTER;
+  }
+}
+
+static void program_params(const hawk_pipeline& p, hk::KParams& kp) {
+  std::memset(&kp, 0, sizeof kp);
+  kp.p = p;
+  kp.npre = compile_filters(p.filter, p.nfilter, kp.pre);
+  kp.npost = compile_filters(p.post, p.npost, kp.post);
+}
+
+int32_t hawk_b200_program_source(const hawk_pipeline* p, const hawk_variant* v, char* buf,
+                                 int32_t len) {
+  if (!p || !v || !buf || len <= 0) return HAWK_ERR_ARGUMENT;
+  hk::KParams kp;
+  program_params(*p, kp);
+  const std::string s = hk::jit_source(kp, main_role(*p, *v), *v);
+  std::strncpy(buf, s.c_str(), (size_t)len - 1);
+  buf[len - 1] = 0;
+  return (int32_t)s.size() < len ? HAWK_OK : HAWK_ERR_ARGUMENT;
+}
+
+int32_t hawk_b200_program_compile(const hawk_pipeline* p, const hawk_variant* v, char* log,
+                                  int32_t len, size_t* cubin_bytes) {
+  if (!p || !v) return HAWK_ERR_ARGUMENT;
+  hk::KParams kp;
+  program_params(*p, kp);
+  std::string err;
+  size_t n = 0;
+  const int32_t st = hk::jit_compile_only(kp, main_role(*p, *v), *v, &n, &err);
+  if (cubin_bytes) *cubin_bytes = n;
+  if (log && len > 0) {
+    std::strncpy(log, err.c_str(), (size_t)len - 1);
+    log[len - 1] = 0;
+  }
+  return st;
+}
+
 int32_t hawk_b200_ctx_set_option(hawk_ctx* ctx, const char* name, int64_t value) {
   if (!ctx || !name) return HAWK_ERR_ARGUMENT;
   if (std::strcmp(name, "prefetch_passes") == 0) {
     ctx->prefetch_passes = (int)std::max<int64_t>(0, std::min<int64_t>(value, 16));
+    return HAWK_OK;
+  }
+  if (std::strcmp(name, "jit") == 0) {
+    ctx->jit = value != 0;
+    return HAWK_OK;
+  }
+  if (std::strcmp(name, "stage") == 0) {
+    ctx->stage = value != 0;
     return HAWK_OK;
   }
   if (std::strcmp(name, "priv_groups") == 0) {

@@ -3,7 +3,9 @@
 // and mbarriers (sm_90+/sm_100a), warp helpers.
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cstdint>
+#endif
 
 #include "hawk_b200.h"
 

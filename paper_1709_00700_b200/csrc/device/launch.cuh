@@ -12,6 +12,7 @@ namespace hk {
 struct LaunchShape {
   dim3 grid, block;
   size_t smem;
+  void* jit_fn = nullptr;  // compiled program (jit.cu) instead of the AOT instantiation
 };
 
 template <int ROLE, int A, int P, int I, int H, int U>

@@ -64,6 +64,238 @@ __device__ __forceinline__ void evaluate(const KParams& kp, const Batch<R, ACCES
   }
 }
 
+// A program policy gives the kernel skeleton the per-row op chain and the
+// sink inputs. InterpProg interprets the lowered program from the kernel
+// parameters (the AOT instantiations in libhawk_b200.so); a compiled policy
+// (jit.cpp) is generated per pipeline with the same interface, constants
+// inlined and per-row values in registers.
+struct InterpProg {
+  static constexpr bool kStatic = false;  // program shape known only at run time
+  template <int R>
+  struct Vals {};
+  template <int ACCESS, int PRED, int IMPL, int HFN, int R>
+  __device__ static __forceinline__ void eval(const KParams& kp, const Batch<R, ACCESS>& b,
+                                              State<R>& s, Vals<R>&) {
+    evaluate<ACCESS, PRED, IMPL, HFN, R>(kp, b, s);
+  }
+  template <int ACCESS, int PRED, int R>
+  __device__ static __forceinline__ void agg_input(const KParams& kp, int a,
+                                                   const Batch<R, ACCESS>& b, const State<R>& s,
+                                                   const Vals<R>&, u64 (&v)[R]) {
+    fetch<PRED, R, ACCESS>(kp, kp.p.aggs[a].input, kp.p.aggs[a].type, b, s, v);
+  }
+  template <int ACCESS, int PRED, int R>
+  __device__ static __forceinline__ void key_input(const KParams& kp, int i,
+                                                   const Batch<R, ACCESS>& b, const State<R>& s,
+                                                   const Vals<R>&, u64 (&v)[R]) {
+    fetch<PRED, R, ACCESS>(kp, kp.p.keys[i], HAWK_I64, b, s, v);
+  }
+  template <int ACCESS, int PRED, int R>
+  __device__ static __forceinline__ void proj_input(const KParams& kp, int i,
+                                                    const Batch<R, ACCESS>& b, const State<R>& s,
+                                                    const Vals<R>&, u64 (&v)[R]) {
+    fetch<PRED, R, ACCESS>(kp, kp.p.project[i], kp.p.project[i].type, b, s, v);
+  }
+};
+
+// ---- sinks of compiled programs: the shape (keys, aggregates, functions) is
+// static, so keys stay in registers and every aggregate update is specialised
+
+template <int V>
+struct IntC {
+  static constexpr int value = V;
+};
+template <int I, int N>
+struct StaticFor {
+  template <class F>
+  __device__ __forceinline__ static void run(F&& f) {
+    if constexpr (I < N) {
+      f(IntC<I>{});
+      StaticFor<I + 1, N>::run(f);
+    }
+  }
+};
+
+// agg_find_or_insert with K keys held in registers
+template <int IMPL, int HFN, bool SHARED, int K>
+__device__ __forceinline__ u64* agg_find_static(const KParams& kp, u64* slots, int log2cap,
+                                               const uint64_t* seeds, const u64 (&key)[K],
+                                               u64* fresh_counter, int* out_pos) {
+  const hawk_pipeline& p = kp.p;
+  const int words = 1 + K + p.naggs;
+  u64 x = key[0];
+#pragma unroll
+  for (int i = 1; i < K; ++i) x = combine_key(x, key[i]);
+  const u64 h = HFN == HAWK_MURMUR ? fmix64(x ^ seeds[0]) : ms_multiplier(seeds[0]) * x;
+  const u64 tag = h | 1ull;
+  const u64 cap = 1ull << log2cap;
+  const int max_tries = IMPL == HAWK_LINEAR_PROBING ? (int)(cap < 4096 ? cap : 4096) : 2;
+  u64 pos = HFN == HAWK_MURMUR ? (h & (cap - 1ull)) : (h >> (64 - log2cap));
+  for (int t = 0; t < max_tries; ++t) {
+    if (IMPL == HAWK_CUCKOO && t == 1) pos = cap + hash_slot<HFN>(x, seeds[1], log2cap);
+    u64* sl = slots + pos * (u64)words;
+    u64 st = SHARED ? ld_acquire_cta(sl) : ld_acquire_gpu(sl);
+    if (st == 0ull) {
+      const u64 prev = atomicCAS(sl, 0ull, kBusy);
+      if (prev == 0ull) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) sl[1 + i] = key[i];
+        for (int a = 0; a < p.naggs; ++a) sl[1 + K + a] = agg_identity(p.aggs[a].fn, p.aggs[a].type);
+        if (SHARED) __threadfence_block(); else __threadfence();
+        atomicExch(sl, tag);
+        if (fresh_counter) atomicAdd(fresh_counter, 1ull);
+        if (out_pos) *out_pos = (int)pos;
+        return sl;
+      }
+      st = prev;
+    }
+    while (st == kBusy) st = SHARED ? ld_acquire_cta(sl) : ld_acquire_gpu(sl);
+    if (st == tag) {
+      bool eq = true;
+#pragma unroll
+      for (int i = 0; i < K; ++i) eq &= ld_volatile(sl + 1 + i) == key[i];
+      if (eq) {
+        if (out_pos) *out_pos = (int)pos;
+        return sl;
+      }
+    }
+    if (IMPL == HAWK_LINEAR_PROBING) pos = (pos + 1) & (cap - 1ull);
+  }
+  return nullptr;
+}
+
+// Dense group ordinal of a CTA-table slot: exactly one thread per group (the
+// one that moves the slot from -1 to -2) draws the next ordinal.
+__device__ __forceinline__ int claim_ordinal(int* ordinal, int si, int* ord_slot, int* nord, int GP) {
+  volatile int* ov = reinterpret_cast<volatile int*>(ordinal + si);
+  int o = *ov;
+  if (o < 0) {
+    if (o == -1 && atomicCAS(ordinal + si, -1, -2) == -1) {
+      const int mine = atomicAdd(nord, 1);
+      o = mine < GP ? mine : GP;
+      if (o < GP) ord_slot[o] = si;
+      __threadfence_block();
+      *ov = o;
+    } else {
+      while ((o = *ov) < 0) {
+      }
+    }
+  }
+  return o;
+}
+
+template <class P, int ROLE, int ACCESS, int PRED, int IMPL, int HFN, int R>
+__device__ __forceinline__ void hagg_static(const KParams& kp, const Batch<R, ACCESS>& b,
+                                            const State<R>& s,
+                                            const typename P::template Vals<R>& vals,
+                                            u64* local_table, int* ordinal, int* ord_slot,
+                                            int* nord, u64* priv, int GP,
+                                            u64 (&last_key)[HAWK_MAX_KEYS], u64& last_target) {
+  constexpr int K = P::kKeys, A = P::kAggs;
+  const int B = blockDim.x;
+  const uint32_t alive = s.alive;
+  const hawk_table& gt = kp.p.sink_table;
+  u64 key[K][R];
+  StaticFor<0, K>::run([&](auto ic) {
+    constexpr int i = decltype(ic)::value;
+    P::template key_value<i, ACCESS, PRED, R>(kp, b, s, vals, key[i]);
+  });
+  // target per row: private word offset ((ord*A*B + t) << 1 | 1), slot, or 0
+  u64 tw[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    u64 target = 0;
+    if ((alive >> j) & 1u) {
+      u64 kj[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) kj[i] = key[i][j];
+      bool same = last_target != 0;
+#pragma unroll
+      for (int i = 0; i < K; ++i) same &= kj[i] == last_key[i];
+      if (same) {
+        target = last_target;
+      } else {
+        u64* slot = nullptr;
+        if constexpr (ROLE == K_HAGG_LOCAL) {
+          int si = 0;
+          slot = agg_find_static<IMPL, HFN, true, K>(kp, local_table, kp.local_log2, gt.seed, kj,
+                                                     nullptr, &si);
+          if (slot != nullptr && GP > 0) {
+            const int o = claim_ordinal(ordinal, si, ord_slot, nord, GP);
+            if (o < GP) target = ((((u64)o * A * B) + threadIdx.x) << 1) | 1ull;
+          }
+        }
+        if (target == 0) {
+          if (slot == nullptr)
+            slot = agg_find_static<IMPL, HFN, false, K>(kp, reinterpret_cast<u64*>(gt.d_slots),
+                                                        gt.log2_capacity, gt.seed, kj,
+                                                        kp.d_cursor, nullptr);
+          if (slot == nullptr) atomicOr(kp.d_flags, HAWK_FLAG_TABLE_FULL);
+          target = reinterpret_cast<u64>(slot);
+        }
+#pragma unroll
+        for (int i = 0; i < K; ++i) last_key[i] = kj[i];
+        last_target = target;
+      }
+    }
+    tw[j] = target;
+  }
+  StaticFor<0, A>::run([&](auto ac) {
+    constexpr int a = decltype(ac)::value;
+    constexpr int fn = P::kAggFn[a], ty = P::kAggType[a];
+    u64 v[R];
+    if constexpr (fn == HAWK_COUNT) {
+#pragma unroll
+      for (int j = 0; j < R; ++j) v[j] = 1ull;
+    } else {
+      P::template agg_value<a, ACCESS, PRED, R>(kp, b, s, vals, v);
+    }
+    u64* pa = priv + (size_t)a * B;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      if (tw[j] & 1ull) {
+        u64& acc = pa[tw[j] >> 1];
+        if constexpr (fn == HAWK_COUNT || (fn == HAWK_SUM && ty == HAWK_I64)) acc += v[j];
+        else acc = agg_combine(fn, ty, acc, v[j]);
+      } else if (tw[j]) {
+        agg_update(reinterpret_cast<u64*>(tw[j]) + 1 + K + a, fn, ty, v[j]);
+      }
+    }
+  });
+}
+
+template <class P, int ACCESS, int PRED, int R>
+__device__ __forceinline__ void agg_static(const KParams& kp, const Batch<R, ACCESS>& b,
+                                           State<R>& s, const typename P::template Vals<R>& vals) {
+  const uint32_t alive = s.alive;
+  StaticFor<0, P::kAggs>::run([&](auto ac) {
+    constexpr int a = decltype(ac)::value;
+    constexpr int fn = P::kAggFn[a], ty = P::kAggType[a];
+    u64& acc = s.acc(a);
+    if constexpr (fn == HAWK_COUNT) {
+      acc += (u64)__popc(alive);
+    } else {
+      u64 v[R];
+      P::template agg_value<a, ACCESS, PRED, R>(kp, b, s, vals, v);
+      if constexpr (fn == HAWK_SUM && ty == HAWK_I64) {
+        u64 sum = 0;
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          if (PRED == HAWK_PREDICATED) sum += v[j] * (u64)((alive >> j) & 1u);
+          else if ((alive >> j) & 1u) sum += v[j];
+        }
+        acc += sum;
+      } else {
+        u64 x = acc;
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+          if ((alive >> j) & 1u) x = agg_combine(fn, ty, x, v[j]);
+        acc = x;
+      }
+    }
+  });
+}
+
 // block-wide exclusive scan of one 64-bit value per thread; returns the
 // exclusive prefix and writes the block total. Uses `scratch` (>= 33 words).
 __device__ __forceinline__ u64 block_exclusive_scan(u64 v, u64* scratch, u64& total) {
@@ -87,10 +319,10 @@ __device__ __forceinline__ u64 block_exclusive_scan(u64 v, u64* scratch, u64& to
 }
 
 
-template <int ROLE, int ACCESS, int PRED, int IMPL, int HFN, int U>
-__global__ void __launch_bounds__(kMaxBlock, U == 1 ? 3 : (U == 2 ? 2 : 1))
-    pipeline_kernel(const __grid_constant__ KParams kp) {
+template <class P, int ROLE, int ACCESS, int PRED, int IMPL, int HFN, int U>
+__device__ __forceinline__ void pipeline_body(const KParams& kp) {
   constexpr int R = 4 * U;
+  typename P::template Vals<R> vals;
   extern __shared__ __align__(128) unsigned char smem[];
   const hawk_pipeline& p = kp.p;
   const int B = blockDim.x;
@@ -144,12 +376,16 @@ __global__ void __launch_bounds__(kMaxBlock, U == 1 ? 3 : (U == 2 ? 2 : 1))
   u64 last_target = 0;
 
   auto process = [&](const Batch<R, ACCESS>& b) {
-    evaluate<ACCESS, PRED, IMPL, HFN, R>(kp, b, s);
+    P::template eval<ACCESS, PRED, IMPL, HFN, R>(kp, b, s, vals);
     const uint32_t alive = s.alive;
     if constexpr (ROLE == K_AGG_LOCAL || ROLE == K_AGG_GLOBAL) {
       // AGGREGATE: predicated SUM/COUNT multiply by the
       // 0/1 result_increment, MIN/MAX select.
       if (PRED == HAWK_BRANCHED && alive == 0u) return;
+      if constexpr (P::kStatic) {
+        agg_static<P, ACCESS, PRED, R>(kp, b, s, vals);
+        return;
+      }
       for (int a = 0; a < p.naggs; ++a) {
         const hawk_agg& g = p.aggs[a];
         u64& acc = s.acc(a);
@@ -158,7 +394,7 @@ __global__ void __launch_bounds__(kMaxBlock, U == 1 ? 3 : (U == 2 ? 2 : 1))
           continue;
         }
         u64 v[R];
-        fetch<PRED, R, ACCESS>(kp, g.input, g.type, b, s, v);
+        P::template agg_input<ACCESS, PRED, R>(kp, a, b, s, vals, v);
         if (g.fn == HAWK_SUM && g.type == HAWK_I64) {
           u64 sum = 0;
 #pragma unroll
@@ -177,9 +413,15 @@ __global__ void __launch_bounds__(kMaxBlock, U == 1 ? 3 : (U == 2 ? 2 : 1))
       }
     } else if constexpr (ROLE == K_HAGG_LOCAL || ROLE == K_HAGG_GLOBAL) {
       if (PRED == HAWK_BRANCHED && alive == 0u) return;
+      if constexpr (P::kStatic) {
+        hagg_static<P, ROLE, ACCESS, PRED, IMPL, HFN, R>(kp, b, s, vals, local_table, ordinal,
+                                                         ord_slot, nord, priv, GP, last_key,
+                                                         last_target);
+        return;
+      }
       for (int i = 0; i < K; ++i) {
         u64 v[R];
-        fetch<PRED, R, ACCESS>(kp, p.keys[i], HAWK_I64, b, s, v);
+        P::template key_input<ACCESS, PRED, R>(kp, i, b, s, vals, v);
 #pragma unroll
         for (int j = 0; j < R; ++j) s.key(i, j) = v[j];
       }
@@ -261,7 +503,7 @@ __global__ void __launch_bounds__(kMaxBlock, U == 1 ? 3 : (U == 2 ? 2 : 1))
 #pragma unroll
             for (int j = 0; j < R; ++j) v[j] = 1ull;
           } else {
-            fetch<PRED, R, ACCESS>(kp, g.input, g.type, b, s, v);
+            P::template agg_input<ACCESS, PRED, R>(kp, a, b, s, vals, v);
           }
 #pragma unroll
           for (int j = 0; j < R; ++j) {
@@ -270,7 +512,7 @@ __global__ void __launch_bounds__(kMaxBlock, U == 1 ? 3 : (U == 2 ? 2 : 1))
           }
         } else {
           u64 v[R];
-          fetch<PRED, R, ACCESS>(kp, g.input, g.type, b, s, v);
+          P::template agg_input<ACCESS, PRED, R>(kp, a, b, s, vals, v);
 #pragma unroll
           for (int j = 0; j < R; ++j) {
             if (tw[j] & 1ull) {
@@ -296,7 +538,7 @@ __global__ void __launch_bounds__(kMaxBlock, U == 1 ? 3 : (U == 2 ? 2 : 1))
         const u64 pos = base + incl - cnt;
         for (int i = 0; i < p.nproject; ++i) {
           u64 v[R];
-          fetch<PRED, R, ACCESS>(kp, p.project[i], p.project[i].type, b, s, v);
+          P::template proj_input<ACCESS, PRED, R>(kp, i, b, s, vals, v);
           int64_t* out = kp.d_out + (size_t)i * kp.out_stride + pos;
           int k = 0;
 #pragma unroll
@@ -314,7 +556,7 @@ __global__ void __launch_bounds__(kMaxBlock, U == 1 ? 3 : (U == 2 ? 2 : 1))
         const u64 pos = scatter_base + running + excl;
         for (int i = 0; i < p.nproject; ++i) {
           u64 v[R];
-          fetch<PRED, R, ACCESS>(kp, p.project[i], p.project[i].type, b, s, v);
+          P::template proj_input<ACCESS, PRED, R>(kp, i, b, s, vals, v);
           int64_t* out = kp.d_out + (size_t)i * kp.out_stride + pos;
           int k = 0;
 #pragma unroll
@@ -326,7 +568,7 @@ __global__ void __launch_bounds__(kMaxBlock, U == 1 ? 3 : (U == 2 ? 2 : 1))
     } else if constexpr (ROLE == K_PUT_SINGLE) {
       if (PRED == HAWK_BRANCHED && alive == 0u) return;
       u64 key[R];
-      fetch<PRED, R, ACCESS>(kp, p.keys[0], HAWK_I64, b, s, key);
+      P::template key_input<ACCESS, PRED, R>(kp, 0, b, s, vals, key);
 #pragma unroll
       for (int j = 0; j < R; ++j)
         if ((alive >> j) & 1u)
@@ -496,6 +738,12 @@ __global__ void __launch_bounds__(kMaxBlock, U == 1 ? 3 : (U == 2 ? 2 : 1))
     block_exclusive_scan(count, scratch, total);
     if (threadIdx.x == 0) kp.d_offsets[blockIdx.x] = (int64_t)total;
   }
+}
+
+template <int ROLE, int ACCESS, int PRED, int IMPL, int HFN, int U>
+__global__ void __launch_bounds__(kMaxBlock, U == 1 ? 3 : (U == 2 ? 2 : 1))
+    pipeline_kernel(const __grid_constant__ KParams kp) {
+  pipeline_body<InterpProg, ROLE, ACCESS, PRED, IMPL, HFN, U>(kp);
 }
 
 }  // namespace hk

@@ -307,6 +307,45 @@ int32_t hawk_engine_validate(hawk_engine* e, const char* sql, const char* config
   });
 }
 
+// Generates and NVRTC-compiles the program of every pipeline (no GPU needed);
+// `buf` receives one line per pipeline ("<i> ok <cubin bytes>" or the log).
+int32_t hawk_engine_compile_check(hawk_engine* e, const char* sql, const char* config, char* buf,
+                                  int32_t len) {
+  return guard([&] {
+    PipelineSet set = plan_sql(e->engine, sql);
+    auto configs = configs_for(set, config ? config : "");
+    std::vector<HashTableDescriptor> desc;
+    std::vector<VariantConfiguration> eff;
+    std::vector<PipelineProgram> progs = apply_variants(set, configs, desc, &eff);
+    std::ostringstream os;
+    bool all_ok = true;
+    for (std::size_t i = 0; i < progs.size(); ++i) {
+      LoweredProgram lp = lower_program(progs[i], set);
+      hawk_variant v{};
+      v.strategy = static_cast<int32_t>(eff[i].strategy);
+      v.memory_access = static_cast<int32_t>(eff[i].memory_access);
+      v.predication = static_cast<int32_t>(eff[i].predication);
+      v.hash_table_impl = static_cast<int32_t>(eff[i].hash_table_impl);
+      v.hash_function = static_cast<int32_t>(eff[i].hash_function);
+      v.thread_multiplier = eff[i].thread_multiplier;
+      v.work_group_size = eff[i].work_group_size;
+      v.hash_table_count_multiplier = eff[i].hash_table_count_multiplier;
+      v.unroll_factor = lp.unroll;
+      std::string log(8192, '\0');
+      size_t bytes = 0;
+      const int32_t st = hawk_b200_program_compile(&lp.pipe, &v, log.data(), (int32_t)log.size(), &bytes);
+      if (st == HAWK_OK) {
+        os << i << " ok " << bytes << "\n";
+      } else {
+        all_ok = false;
+        os << i << " error " << st << " " << log.c_str() << "\n";
+      }
+    }
+    put_str(buf, len, os.str());
+    if (!all_ok) throw Error("program compilation failed:\n" + os.str());
+  });
+}
+
 int32_t hawk_engine_explain(hawk_engine* e, const char* sql, const char* config, char* buf,
                             int32_t len) {
   return guard([&] {

@@ -294,6 +294,19 @@ class Engine:
         _check(self._lib.hawk_engine_validate(self._h, sql.encode(), config.encode(), buf, 1 << 16))
         return buf.value.decode()
 
+    def compile_check(self, sql: str, config: str = "") -> str:
+        """NVRTC-compiles every pipeline's generated program (no GPU needed)."""
+        buf = C.create_string_buffer(1 << 16)
+        _check(self._lib.hawk_engine_compile_check(self._h, sql.encode(), config.encode(), buf,
+                                                   1 << 16))
+        return buf.value.decode()
+
+    def set_option(self, name: str, value: int):
+        """Context knobs of libhawk_b200 (hawk_b200_ctx_set_option): jit, prefetch_passes, ..."""
+        st = _native.b200().hawk_b200_ctx_set_option(self.ctx, name.encode(), int(value))
+        if st != 0:
+            raise InvalidParams(f"option {name}={value}: status {st}")
+
     def explain(self, sql: str, config: str = "") -> str:
         buf = C.create_string_buffer(1 << 16)
         _check(self._lib.hawk_engine_explain(self._h, sql.encode(), config.encode(), buf, 1 << 16))
