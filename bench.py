@@ -27,10 +27,10 @@ METRIC = "input tuples/sec & HBM GB/s (roofline frac) per TPC-H/SSB query, 1/2/4
 
 # learned/selected variant per query (--config overrides)
 DEFAULT_CONFIG = {
-    "tpch_q6": "multi_pass/coalesced/branched/tm=1024;local_hash/coalesced/predicated/linear_probing/murmur/wg=256/ht=1",
-    "tpch_q1": "multi_pass/coalesced/branched/tm=1024;local_hash/coalesced/branched/linear_probing/murmur/wg=256/ht=1",
-    "ssb_q11": "single_pass/coalesced/branched;local_hash/coalesced/branched/linear_probing/murmur/wg=256/ht=1",
-    "ssb_q41": "single_pass/coalesced/branched;local_hash/coalesced/branched/linear_probing/murmur/wg=256/ht=1",
+    "tpch_q6": "single_pass/coalesced/branched;global_hash/coalesced/branched/linear_probing/murmur/wg=256",
+    "tpch_q1": "single_pass/coalesced/branched;local_hash/coalesced/branched/linear_probing/murmur/wg=256/ht=8",
+    "ssb_q11": "single_pass/coalesced/branched;global_hash/coalesced/branched/linear_probing/murmur/wg=256",
+    "ssb_q41": "single_pass/coalesced/branched;local_hash/coalesced/branched/linear_probing/murmur/wg=256/ht=8",
     "tpch_q3": "single_pass/coalesced/branched;global_hash/coalesced/branched/linear_probing/murmur/wg=256",
 }
 DEFAULT_SF = {"tpch_q6": 1.0, "tpch_q1": 10.0, "ssb_q11": 10.0, "ssb_q41": 10.0, "tpch_q3": 10.0}

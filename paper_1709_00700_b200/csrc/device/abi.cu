@@ -292,7 +292,7 @@ int32_t prepare(hawk_ctx* ctx, const hawk_pipeline& pipe, const hawk_variant& v,
   shape.jit_fn = nullptr;
   if (ctx->jit) {  // compiled program: generate + NVRTC (cached), see jit.cu
     std::string err;
-    const int32_t st = hk::jit_function(kp, role, v, &shape.jit_fn, &err);
+    const int32_t st = hk::jit_function(kp, role, v, block, &shape.jit_fn, &err);
     if (st != HAWK_OK) {
       fprintf(stderr, "hawk_b200: program compilation failed: %s\n", err.c_str());
       return st;
@@ -301,9 +301,12 @@ int32_t prepare(hawk_ctx* ctx, const hawk_pipeline& pipe, const hawk_variant& v,
   size_t smem = 0;
   // the TMA pipeline gets shallower before the plan is declared too large
   // and finally the tile is read straight from HBM (coalesced, unstaged)
-  while (!layout_smem(ctx, kp, role, v.memory_access, v.hash_table_impl, v.unroll_factor, block,
-                      &smem, shape.jit_fn != nullptr)) {
-    if (v.memory_access == HAWK_COALESCED && kp.prefetch_passes > 1) {
+  // (staging is also dropped when it alone would leave one CTA per SM)
+  for (;;) {
+    const bool fits = layout_smem(ctx, kp, role, v.memory_access, v.hash_table_impl,
+                                  v.unroll_factor, block, &smem, shape.jit_fn != nullptr);
+    if (fits && !(kp.nprefetch > 0 && smem > 100 * 1024)) break;
+    if (!fits && v.memory_access == HAWK_COALESCED && kp.prefetch_passes > 1) {
       --kp.prefetch_passes;
     } else if (v.memory_access == HAWK_COALESCED && kp.nprefetch > 0) {
       kp.nprefetch = 0;

@@ -11,7 +11,7 @@ namespace hk {
 
 // Generates, compiles (NVRTC, sm_100a) and caches the kernel of one pipeline
 // role for one variant point; *fn is a CUfunction.
-int32_t jit_function(const KParams& kp, int role, const hawk_variant& v, void** fn,
+int32_t jit_function(const KParams& kp, int role, const hawk_variant& v, int block, void** fn,
                      std::string* error);
 int32_t jit_occupancy(void* fn, int block, size_t smem, int* ctas);
 int32_t jit_launch(void* fn, const KParams& kp, dim3 grid, dim3 block, size_t smem,

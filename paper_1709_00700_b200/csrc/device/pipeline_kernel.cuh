@@ -71,6 +71,7 @@ __device__ __forceinline__ void evaluate(const KParams& kp, const Batch<R, ACCES
 // inlined and per-row values in registers.
 struct InterpProg {
   static constexpr bool kStatic = false;  // program shape known only at run time
+  static constexpr int kBlock = 0;        // block size known only at run time
   template <int R>
   struct Vals {};
   template <int ACCESS, int PRED, int IMPL, int HFN, int R>
@@ -192,7 +193,7 @@ __device__ __forceinline__ void hagg_static(const KParams& kp, const Batch<R, AC
                                             int* nord, u64* priv, int GP,
                                             u64 (&last_key)[HAWK_MAX_KEYS], u64& last_target) {
   constexpr int K = P::kKeys, A = P::kAggs;
-  const int B = blockDim.x;
+  const int B = P::kBlock > 0 ? P::kBlock : (int)blockDim.x;
   const uint32_t alive = s.alive;
   const hawk_table& gt = kp.p.sink_table;
   u64 key[K][R];
@@ -325,7 +326,7 @@ __device__ __forceinline__ void pipeline_body(const KParams& kp) {
   typename P::template Vals<R> vals;
   extern __shared__ __align__(128) unsigned char smem[];
   const hawk_pipeline& p = kp.p;
-  const int B = blockDim.x;
+  const int B = P::kBlock > 0 ? P::kBlock : (int)blockDim.x;  // static for compiled programs
   const int64_t cb = min(p.nrows, (int64_t)blockIdx.x * kp.chunk_rows);
   const int64_t ce = min(p.nrows, cb + kp.chunk_rows);
   u64* scratch = reinterpret_cast<u64*>(smem + kp.smem_scratch_off);
@@ -613,9 +614,13 @@ __device__ __forceinline__ void pipeline_body(const KParams& kp) {
       b.base = cb + ps * pass_rows;
       b.B = B;
       b.stage = C > 0 ? stages + (size_t)st * C * pass_rows : nullptr;
-      b.valid = 0;
+      if (b.base + pass_rows <= ce) {
+        b.valid = (1u << R) - 1u;
+      } else {
+        b.valid = 0;
 #pragma unroll
-      for (int j = 0; j < R; ++j) b.valid |= (uint32_t)(b.row(j) < ce) << j;
+        for (int j = 0; j < R; ++j) b.valid |= (uint32_t)(b.row(j) < ce) << j;
+      }
       process(b);
       __syncthreads();  // every thread is done with stage st
       if (threadIdx.x == 0 && C > 0 && ps + S < npasses) {
@@ -633,9 +638,13 @@ __device__ __forceinline__ void pipeline_body(const KParams& kp) {
       b.base = ts + k;
       b.B = B;
       b.stage = nullptr;
-      b.valid = 0;
+      if (ts + k + R <= te) {
+        b.valid = (1u << R) - 1u;
+      } else {
+        b.valid = 0;
 #pragma unroll
-      for (int j = 0; j < R; ++j) b.valid |= (uint32_t)(ts + k + j < te) << j;
+        for (int j = 0; j < R; ++j) b.valid |= (uint32_t)(ts + k + j < te) << j;
+      }
       process(b);
     }
   }

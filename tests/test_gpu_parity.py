@@ -42,37 +42,47 @@ def micro(engine):
     return engine, harness.oracle_db(tables)
 
 
+@pytest.mark.parametrize("jit", [1, 0], ids=["compiled", "interpreted"])
 @pytest.mark.parametrize("cfg", CONFIGS)
-def test_micro_queries_all_strategies(micro, cfg):
+def test_micro_queries_all_strategies(micro, cfg, jit):
     engine, db = micro
+    engine.set_option("jit", jit)
     for name, sql in harness.MICRO:
         expected = db.execute(sql)
         got = engine.run(sql, cfg)
         diff = harness.compare(expected, got)
         assert diff is None, f"{name} [{cfg}]: {diff}"
         assert harness.result_table(got).checksum() == expected.checksum(), name
+    engine.set_option("jit", 0)
 
 
-def test_listing2_full_projection_space(micro):
+@pytest.mark.parametrize("jit,stride", [(0, 1), (1, 8)], ids=["interpreted-all", "compiled-sample"])
+def test_listing2_full_projection_space(micro, jit, stride):
     engine, db = micro
+    engine.set_option("jit", jit)
     expected = db.execute(Q.LISTING2)
     n, _ = engine.space_size(Q.LISTING2, 0)
     assert n == 32
-    for i in range(n):
+    for i in range(0, n, stride):
         cfg = engine.space_config(Q.LISTING2, 0, i) + ";" + AGG[0]
         diff = harness.compare(expected, engine.run(Q.LISTING2, cfg))
         assert diff is None, f"{cfg}: {diff}"
+    engine.set_option("jit", 0)
 
 
-def test_listing8_full_aggregation_space(micro):
+@pytest.mark.parametrize("jit,stride", [(0, 1), (1, 57)], ids=["interpreted-all", "compiled-sample"])
+def test_listing8_full_aggregation_space(micro, jit, stride):
+    # every one of the 896 variants interpreted; a strided sample compiled
     engine, db = micro
+    engine.set_option("jit", jit)
     expected = db.execute(Q.LISTING8)
     n, _ = engine.space_size(Q.LISTING8, 0)
     assert n == 896
-    for i in range(n):
+    for i in range(0, n, stride):
         cfg = PROJ[0] + ";" + engine.space_config(Q.LISTING8, 0, i)
         diff = harness.compare(expected, engine.run(Q.LISTING8, cfg))
         assert diff is None, f"{cfg}: {diff}"
+    engine.set_option("jit", 0)
 
 
 @pytest.fixture(scope="module", params=["tpch", "ssb"])
@@ -84,9 +94,11 @@ def bench_db(request):
     e.close()
 
 
+@pytest.mark.parametrize("jit", [1, 0], ids=["compiled", "interpreted"])
 @pytest.mark.parametrize("cfg", CONFIGS)
-def test_baseline_queries_match_oracle(bench_db, cfg):
+def test_baseline_queries_match_oracle(bench_db, cfg, jit):
     which, engine, db = bench_db
+    engine.set_option("jit", jit)
     golden = {g["query"]: g for g in json.load(open(os.path.join(GOLDEN, "bench_sf0.01.json")))}
     for key, sql in harness.BENCH:
         if key.startswith("ssb") != (which == "ssb"):

@@ -102,3 +102,19 @@ def test_cross_join_is_reported_unsupported(micro):
     sql = "select lo_quantity, p_size from part, lineorder where p_size < 2 and lo_quantity < 2"
     with pytest.raises(Unsupported):
         micro.explain(sql, f"{PROJ};{AGG}")
+
+
+@pytest.mark.parametrize("key", [k for k, _ in harness.BENCH])
+def test_compiled_programs_build_for_sm100a(key):
+    # the generated program policy of every pipeline compiles with NVRTC for
+    # sm_100a (code generation is checked here; execution in test_gpu_parity)
+    db_name = "ssb" if key.startswith("ssb") else "tpch"
+    e = _planner(harness.bench_tables(db_name, 0.001, 42))
+    sql = dict(harness.BENCH)[key]
+    for cfg in (f"{PROJ};{AGG}",
+                "multi_pass/coalesced/predicated/tm=1024;"
+                "global_hash/coalesced/predicated/cuckoo/multiply_shift/wg=256"):
+        report = e.compile_check(sql, cfg)
+        lines = [l for l in report.splitlines() if l]
+        assert len(lines) == e.pipeline_count(sql)
+        assert all(" ok " in l for l in lines), report
