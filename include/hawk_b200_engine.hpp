@@ -190,6 +190,10 @@ struct LoweredProgram {
   int unroll = 1;
 };
 LoweredProgram lower_program(const PipelineProgram& program, const PipelineSet& set);
+/// Orders the probe chain by ascending match probability (inner joins
+/// commute; a probe keyed by another probe's payload stays after it), so the
+/// branched variants stop work on a row as early as possible.
+void reorder_probes(LoweredProgram& lp, const std::vector<double>& match_prob);
 /// Human-readable dump of a lowered device program (one op per line).
 std::string describe(const hawk_pipeline& p);
 

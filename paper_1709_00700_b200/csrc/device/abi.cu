@@ -973,8 +973,8 @@ int32_t hawk_b200_run_pipeline(hawk_ctx* ctx, const hawk_pipeline* pipe, const h
       out->stride = out_stride;
       out->width = p.nproject;
       break;
-    case HAWK_SINK_HASH_PUT:
-      out->rows = rows_written;
+    case HAWK_SINK_HASH_PUT:  // rows inserted into the join table
+      out->rows = s == HAWK_MULTI_PASS ? rows_written : (int64_t)ctrl[2];
       break;
   }
   if (metrics) {

@@ -31,11 +31,7 @@ __device__ __forceinline__ void evaluate(const KParams& kp, const Batch<R, ACCES
     fetch<PRED, R, ACCESS>(kp, pr.key, HAWK_I64, b, s, k);
     const hawk_table& t = p.tables[pr.table];
     int32_t r[R];
-#pragma unroll
-    for (int j = 0; j < R; ++j) {
-      const bool act = PRED == HAWK_PREDICATED ? ((b.valid >> j) & 1u) : ((s.alive >> j) & 1u);
-      r[j] = act ? table_find<IMPL, HFN>(t, k[j]) : -1;
-    }
+    table_find_rows<IMPL, HFN, R>(t, k, PRED == HAWK_PREDICATED ? b.valid : s.alive, r);
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       if (r[j] < 0) s.alive &= ~(1u << j);
@@ -567,6 +563,11 @@ __device__ __forceinline__ void pipeline_body(const KParams& kp) {
       }
       running += total;
     } else if constexpr (ROLE == K_PUT_SINGLE) {
+      {  // inserted-row count (the engine orders probes by build selectivity)
+        const unsigned mask = warp_mask();
+        const unsigned n = __reduce_add_sync(mask, (unsigned)__popc(alive));
+        if (lane_id() == 0 && n) atomicAdd(kp.d_cursor, (u64)n);
+      }
       if (PRED == HAWK_BRANCHED && alive == 0u) return;
       u64 key[R];
       P::template key_input<ACCESS, PRED, R>(kp, 0, b, s, vals, key);

@@ -35,6 +35,52 @@ __device__ __forceinline__ int32_t table_find(const hawk_table& t, u64 key) {
   }
 }
 
+// HASH_PROBE of R rows at once: the home slots of every active row (both
+// candidate slots for cuckoo) are loaded before any is inspected, so a warp
+// has R (2R) independent random loads in flight instead of one; only rows
+// whose home slot holds another key continue the linear-probing walk.
+template <int IMPL, int HFN, int R>
+__device__ __forceinline__ void table_find_rows(const hawk_table& t, const u64 (&key)[R],
+                                                uint32_t act, int32_t (&out)[R]) {
+  const u64* s = reinterpret_cast<const u64*>(t.d_slots);
+  u64 k0[R], v0[R], pos[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    pos[j] = hash_slot<HFN>(key[j], t.seed[0], t.log2_capacity);
+    if ((act >> j) & 1u) ldg128(s + 2 * pos[j], k0[j], v0[j]);
+    else k0[j] = kEmpty, v0[j] = 0;
+  }
+  if (IMPL == HAWK_LINEAR_PROBING) {
+    const u64 mask = (u64)t.capacity - 1ull;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      int32_t r = -1;
+      if (((act >> j) & 1u) && key[j] != kEmpty) {
+        u64 k = k0[j], v = v0[j], i = pos[j];
+        while (k != key[j] && k != kEmpty) {
+          i = (i + 1) & mask;
+          ldg128(s + 2 * i, k, v);
+        }
+        r = k == key[j] ? (int32_t)v : -1;
+      }
+      out[j] = r;
+    }
+  } else {
+    u64 k1[R], v1[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const u64 i = hash_slot<HFN>(key[j], t.seed[1], t.log2_capacity);
+      if ((act >> j) & 1u) ldg128(s + 2 * ((u64)t.capacity + i), k1[j], v1[j]);
+      else k1[j] = kEmpty, v1[j] = 0;
+    }
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const bool ok = ((act >> j) & 1u) && key[j] != kEmpty;
+      out[j] = !ok ? -1 : (k0[j] == key[j] ? (int32_t)v0[j] : (k1[j] == key[j] ? (int32_t)v1[j] : -1));
+    }
+  }
+}
+
 // HASH_PUT: LP = CAS-claim the key slot then store the
 // payload; cuckoo = 128-bit exchange with an eviction chain of <= 32.
 template <int IMPL, int HFN>

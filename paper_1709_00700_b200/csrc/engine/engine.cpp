@@ -499,6 +499,7 @@ static QueryRun run_query(Engine& e, Engine::Impl& I, const PipelineSet& set,
   const PipelineProgram& terminal = progs[T];
 
   std::map<int, hawk_table> built;  // descriptor -> join table
+  std::map<int, double> match_prob; // descriptor -> inserted / build-table rows
   std::vector<void*> scratch;       // blocks to return to the pool
   auto cleanup = [&]() {
     for (void* p : scratch) I.release(p);
@@ -557,6 +558,8 @@ static QueryRun run_query(Engine& e, Engine::Impl& I, const PipelineSet& set,
         }
         pm.rows_out = out.rows;
         built[put.descriptor] = t;
+        match_prob[put.descriptor] =
+            out.rows >= 0 && driver.rows > 0 ? static_cast<double>(out.rows) / driver.rows : 1.0;
         break;
       }
       M.pipelines.push_back(pm);
@@ -564,6 +567,11 @@ static QueryRun run_query(Engine& e, Engine::Impl& I, const PipelineSet& set,
 
     // ---- terminal pipeline ----
     LoweredProgram lp = lower_program(terminal, set);
+    {  // most selective join first (foreign-key probes match ~ inserted / build rows)
+      std::vector<double> prob;
+      for (int d : lp.probe_descriptor) prob.push_back(match_prob.count(d) ? match_prob[d] : 1.0);
+      reorder_probes(lp, prob);
+    }
     I.bind_columns(lp, set);
     const DeviceTable& driver = I.device_table(set, terminal.driver_table);
     lp.pipe.nrows = driver.rows;

@@ -261,6 +261,47 @@ std::string describe(const hawk_pipeline& p) {
   return out;
 }
 
+void reorder_probes(LoweredProgram& lp, const std::vector<double>& match_prob) {
+  hawk_pipeline& p = lp.pipe;
+  const int n = p.nprobe;
+  if (n < 2 || static_cast<int>(match_prob.size()) != n) return;
+  // greedy: the most selective probe whose key is available goes next
+  std::vector<int> perm, inv(static_cast<std::size_t>(n), -1);
+  std::vector<bool> placed(static_cast<std::size_t>(n), false);
+  for (int k = 0; k < n; ++k) {
+    int best = -1;
+    for (int i = 0; i < n; ++i) {
+      if (placed[static_cast<std::size_t>(i)]) continue;
+      const hawk_operand& key = p.probe[i].key;
+      if (key.kind == HAWK_OPND_PAYLOAD && !placed[static_cast<std::size_t>(key.probe)]) continue;
+      if (best < 0 || match_prob[static_cast<std::size_t>(i)] < match_prob[static_cast<std::size_t>(best)])
+        best = i;
+    }
+    if (best < 0) return;  // cyclic payload keys: keep the lowering's order
+    placed[static_cast<std::size_t>(best)] = true;
+    inv[static_cast<std::size_t>(best)] = k;
+    perm.push_back(best);
+  }
+  auto remap = [&](hawk_operand& o) {
+    if (o.kind == HAWK_OPND_PAYLOAD) o.probe = inv[static_cast<std::size_t>(o.probe)];
+  };
+  hawk_probe old[HAWK_MAX_PROBES];
+  std::vector<int> old_desc = lp.probe_descriptor;
+  for (int i = 0; i < n; ++i) old[i] = p.probe[i];
+  for (int k = 0; k < n; ++k) {
+    p.probe[k] = old[perm[static_cast<std::size_t>(k)]];
+    p.probe[k].table = k;
+    remap(p.probe[k].key);
+    lp.probe_descriptor[static_cast<std::size_t>(k)] = old_desc[static_cast<std::size_t>(perm[static_cast<std::size_t>(k)])];
+  }
+  for (int i = 0; i < p.nfilter; ++i) remap(p.filter[i].lhs), remap(p.filter[i].rhs);
+  for (int i = 0; i < p.npost; ++i) remap(p.post[i].lhs), remap(p.post[i].rhs);
+  for (int i = 0; i < p.narith; ++i) remap(p.arith[i].lhs), remap(p.arith[i].rhs);
+  for (int i = 0; i < p.nkeys; ++i) remap(p.keys[i]);
+  for (int i = 0; i < p.naggs; ++i) remap(p.aggs[i].input);
+  for (int i = 0; i < p.nproject; ++i) remap(p.project[i]);
+}
+
 LoweredProgram lower_program(const PipelineProgram& program, const PipelineSet& set) {
   Lowerer l(program, set);
   l.run();
