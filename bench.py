@@ -27,11 +27,11 @@ METRIC = "input tuples/sec & HBM GB/s (roofline frac) per TPC-H/SSB query, 1/2/4
 
 # learned/selected variant per query (--config overrides)
 DEFAULT_CONFIG = {
-    "tpch_q6": "single_pass/coalesced/branched;global_hash/coalesced/branched/linear_probing/murmur/wg=256",
-    "tpch_q1": "single_pass/coalesced/branched;local_hash/coalesced/branched/linear_probing/murmur/wg=256/ht=8",
-    "ssb_q11": "single_pass/coalesced/branched;global_hash/coalesced/branched/linear_probing/murmur/wg=256",
-    "ssb_q41": "single_pass/coalesced/branched;local_hash/coalesced/branched/linear_probing/murmur/wg=256/ht=8",
-    "tpch_q3": "single_pass/coalesced/branched;global_hash/coalesced/branched/linear_probing/murmur/wg=256",
+    "tpch_q6": "single_pass/sequential/branched/u=2;global_hash/sequential/branched/linear_probing/multiply_shift/wg=256/u=2",
+    "tpch_q1": "single_pass/coalesced/branched;local_hash/coalesced/predicated/linear_probing/murmur/wg=256/ht=8",
+    "ssb_q11": "single_pass/coalesced/branched;global_hash/coalesced/branched/linear_probing/multiply_shift/wg=256",
+    "ssb_q41": "single_pass/coalesced/branched;global_hash/coalesced/branched/cuckoo/multiply_shift/wg=256",
+    "tpch_q3": "single_pass/coalesced/branched/u=2;global_hash/coalesced/branched/linear_probing/multiply_shift/wg=256",
 }
 DEFAULT_SF = {"tpch_q6": 1.0, "tpch_q1": 10.0, "ssb_q11": 10.0, "ssb_q41": 10.0, "tpch_q3": 10.0}
 WORKLOAD_NAME = {"tpch_q6": "TPC-H Q6", "tpch_q1": "TPC-H Q1", "ssb_q11": "SSB Q1.1",
@@ -53,8 +53,15 @@ def parse():
     ap.add_argument("--cpu-sample-rows", type=int, default=4_000_000)
     ap.add_argument("--prefetch", type=int, default=None, help="TMA pipeline depth (pass tiles)")
     ap.add_argument("--stage", type=int, default=1, help="1: TMA-staged pass tiles (coalesced)")
+    ap.add_argument("--pass-sync", type=int, default=None,
+                    help="unstaged coalesced tiles: CTA barrier after every pass (1) or not (0)")
+    ap.add_argument("--l2-distance", type=int, default=None,
+                    help="unstaged coalesced tiles: L2 bulk-prefetch distance (passes, 0 = off)")
     ap.add_argument("--jit", type=int, default=1,
                     help="1: compiled programs (NVRTC), 0: the AOT interpreter instantiations")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="exchange backend for N>1 (gloo: host-side exchange, for checking the "
+                         "multi-rank path when fewer GPUs than ranks are visible)")
     ap.add_argument("--sweep", nargs="*", default=None,
                     help="time each given config (or a built-in list) and print one line per config")
     return ap.parse_args()
@@ -90,6 +97,10 @@ def run_sweep(args):
         engine.set_option("prefetch_passes", args.prefetch)
     engine.set_option("jit", args.jit)
     engine.set_option("stage", args.stage)
+    if args.l2_distance is not None:
+        engine.set_option("l2_distance", args.l2_distance)
+    if args.pass_sync is not None:
+        engine.set_option("pass_sync", args.pass_sync)
     load_tables(engine, query, sf, args.seed, 0, 1)
     sql = Q.BENCH[query][0]
     for cfg in (args.sweep or SWEEP):
@@ -294,8 +305,12 @@ def main():
     import torch
     if world > 1:
         import torch.distributed as dist
+        local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     from paper_1709_00700_b200 import Engine, _native
     from paper_1709_00700_b200 import datagen as dg
     from paper_1709_00700_b200 import queries as Q
@@ -308,6 +323,10 @@ def main():
     engine = Engine(local)
     engine.set_option("jit", args.jit)
     engine.set_option("stage", args.stage)
+    if args.l2_distance is not None:
+        engine.set_option("l2_distance", args.l2_distance)
+    if args.pass_sync is not None:
+        engine.set_option("pass_sync", args.pass_sync)
     per_rank = load_tables(engine, query, sf, args.seed, rank, world)
     lib = _native.b200()
     stream = torch.cuda.ExternalStream(lib.hawk_b200_ctx_stream(engine.ctx), device=torch.device("cuda", local))
@@ -316,17 +335,23 @@ def main():
     alg_bytes = algorithmic_bytes(query, per_rank, dims)
     flush = alg_bytes < 4 * l2
 
+    xdev = torch.device("cuda", local) if args.backend == "nccl" else torch.device("cpu")
+
     def step():
+        """One query: (result, kernels launched). N>1: shard partials, NCCL
+        all-gather of the partial rows, device merge + finalise."""
         if world == 1:
-            return engine.run(sql, cfg)
-        parts, sink, _ = engine.run_partial(sql, cfg)
-        gathered = all_gather_rows(parts, device=torch.device("cuda", local))
-        return engine.finalize(sql, gathered, cfg)
+            r = engine.run(sql, cfg)
+            return r, r.launches
+        part = engine.run_partial(sql, cfg)
+        gathered = all_gather_rows(part.rows, device=xdev)
+        r = engine.finalize(sql, gathered, cfg)
+        return r, part.launches + r.launches
 
     for _ in range(args.warmup):
         if flush:
             engine.flush_l2()
-        r = step()
+        r, _ = step()
     kernel_ms, launches = [], 0
     if world > 1:
         torch.distributed.barrier()
@@ -338,15 +363,15 @@ def main():
             if flush:
                 engine.flush_l2()
             start.record(stream)
-            r = step()
+            r, n_launch = step()
             end.record(stream)
             end.synchronize()
             total_ms += start.elapsed_time(end)
             kernel_ms.append(r.kernel_ms if world == 1 else 0.0)
-            launches += r.launches if world == 1 else 0
+            launches += n_launch
     torch.cuda.synchronize()
     if world > 1:
-        t = torch.tensor([total_ms], device="cuda")
+        t = torch.tensor([total_ms], device=xdev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
@@ -387,8 +412,8 @@ def main():
                             "kernel_ms": term_only_ms, "peak_kind": peak_kind}
     line["clocks"] = clocks.summary()
 
-    if world == 1 and rank == 0 and not args.no_e2e:
-        line["e2e"] = e2e_measure(engine, query, sf, args, cfg)
+    if not args.no_e2e:
+        line["e2e"] = e2e_measure(engine, query, sf, args, step, rank, world, per_rank)
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         n_fact, times = cpu_reference_sample(query, sf, args.seed, args.cpu_sample_rows, reps=1)
         ref_rate = n_fact / times[0]
@@ -408,42 +433,45 @@ def main():
         torch.distributed.destroy_process_group()
 
 
-def e2e_measure(engine, query, sf, args, cfg):
+def e2e_measure(engine, query, sf, args, step, rank, world, per_rank):
     """Same metric through the engine's C ABI with HOST inputs: each step copies
-    the fact table's referenced columns from pinned host memory (H2D), runs the
-    query and reads the result back (D2H)."""
+    this rank's fact-table shard (the referenced columns) from pinned host
+    memory into HBM (hawk_engine_put_columns), runs the query (N>1: partials,
+    NCCL all-gather, merge) and reads the result back (D2H). Timed per step as
+    the max over ranks."""
     import ctypes as C
 
     import numpy as np
-    from paper_1709_00700_b200 import Engine, _native
+    import torch
+    from paper_1709_00700_b200 import _native
     from paper_1709_00700_b200 import datagen as dg
     from paper_1709_00700_b200 import queries as Q
     from paper_1709_00700_b200.engine import INT64, Column
     lib = _native.b200()
-    sql, tables, fact = Q.BENCH[query]
+    _, _, fact = Q.BENCH[query]
     name, schema = dg.SCHEMA[fact]
-    n = dg.table_rows(fact, sf)
+    global_sf = sf * world
+    n = per_rank
     wanted = Q.FACT_COLUMNS[query]
-    host = []
-    pinned = []
-    domains = []
+    host, pinned, domains = [], [], []
     for ci, (cname, lex) in enumerate(schema):
         if cname not in wanted:
             continue
-        domains.append(lib.hawk_b200_gen_column_domain(fact, ci, sf))
+        domains.append(lib.hawk_b200_gen_column_domain(fact, ci, global_sf))
         p = C.c_void_p()
         assert lib.hawk_b200_host_alloc(n * 8, C.byref(p)) == 0
         pinned.append(p)
         arr = np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_int64)), shape=(n,))
-        arr[:] = dg.gen_column(fact, ci, sf, args.seed, 0, n)
+        arr[:] = dg.gen_column(fact, ci, global_sf, args.seed, rank * n, n)
         host.append(Column(cname, INT64 if lex is None else 2, arr, None if lex is None else lex))
     engine.drop(name)
-    times, h2d = [], sum(c.values.nbytes for c in host)
-    d2h = 0
+    times, h2d, d2h = [], sum(c.values.nbytes for c in host), 0
     for i in range(args.warmup + args.steps):
+        if world > 1:
+            torch.distributed.barrier()
         t0 = time.perf_counter()
-        engine.put_table(name, host, distinct=domains)
-        r = engine.run(sql, cfg)
+        engine.put_table(name, host, distinct=domains, row_offset=rank * n)
+        r, _ = step()
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
@@ -451,9 +479,14 @@ def e2e_measure(engine, query, sf, args, cfg):
     for p in pinned:
         lib.hawk_b200_host_free(p)
     ms = statistics.mean(times) * 1e3
-    return {"value": n / (ms / 1e3), "unit": "tuples/s", "h2d_bytes_per_step": h2d,
+    if world > 1:
+        t = torch.tensor([ms], device="cuda" if torch.distributed.get_backend() == "nccl" else "cpu")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"value": n * world / (ms / 1e3), "unit": "tuples/s", "h2d_bytes_per_step": h2d * world,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms,
-            "path": "hawk_engine_put_columns (pinned host -> HBM) + hawk_engine_run (C ABI)"}
+            "path": "hawk_engine_put_columns (pinned host -> HBM) + hawk_engine_run (C ABI)"
+                    + (" / run_partial + NCCL all-gather + finalize" if world > 1 else "")}
 
 
 if __name__ == "__main__":

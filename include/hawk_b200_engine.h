@@ -62,6 +62,7 @@ int32_t hawk_partial_width(const hawk_partial* p);
 int32_t hawk_partial_sink(const hawk_partial* p);
 const int64_t* hawk_partial_data(const hawk_partial* p);
 double hawk_partial_kernel_ms(const hawk_partial* p);
+int32_t hawk_partial_launches(const hawk_partial* p); /* kernels the shard run launched */
 void hawk_partial_free(hawk_partial* p);
 /* merges partial row blocks (each rows[i] x width int64 words) and finalises */
 int32_t hawk_engine_finalize(hawk_engine* e, const char* sql, const char* config, int32_t nparts,

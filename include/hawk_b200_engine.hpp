@@ -74,6 +74,8 @@ struct DeviceColumn {
   ColumnKind kind = ColumnKind::Int64;
   int64_t* d_data = nullptr;  // 8 bytes per row, padded to a multiple of 64 rows
   int64_t distinct = 0;       // exact or upper bound on distinct values; 0 = unknown
+  bool range_known = false;   // [lo, hi] computed on the device on first use as a group key
+  int64_t lo = 0, hi = 0;
 };
 
 struct DeviceTable {

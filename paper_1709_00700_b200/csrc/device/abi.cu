@@ -22,7 +22,11 @@ struct hawk_ctx {
   cudaStream_t stream = nullptr;
   int sms = 148;
   int smem_optin = 227 * 1024;
-  int prefetch_passes = 2;  // COALESCED: L2 bulk-prefetch distance in passes
+  int prefetch_passes = 2;  // COALESCED: TMA pipeline depth in pass tiles
+  int l2_distance = 0;      // COALESCED, unstaged: L2 bulk-prefetch distance in passes
+  int pass_sync = 1;        // COALESCED, unstaged: CTA barrier after every pass tile
+  int stage_probes = 0;     // COALESCED pipelines with probes: TMA staging + barrier too
+  int dense_keys = 1;       // HAGG_LOCAL compiled: dense key-index lookaside when provided
   int priv_groups = 64;     // HAGG_LOCAL: groups with thread-private accumulators
   int jit = 0;              // compiled programs (jit.cu) instead of the interpreter
   int stage = 1;            // COALESCED: stage pass tiles in smem with TMA
@@ -220,6 +224,7 @@ bool layout_smem(hawk_ctx* ctx, hk::KParams& kp, int role, int access, int impl,
   kp.smem_state_off = (int)off;
   off += state_bytes;
   kp.priv_groups = 0;
+  kp.smem_dense_off = 0;
   kp.smem_ord_off = kp.smem_priv_off = (int)off;
   if (role == hk::K_HAGG_LOCAL && p.naggs > 0 && ctx->priv_groups > 0) {
     // thread-private accumulators for the first GP groups of each CTA
@@ -236,6 +241,12 @@ bool layout_smem(hawk_ctx* ctx, hk::KParams& kp, int role, int access, int impl,
       kp.smem_priv_off = (int)off;
       off += (size_t)gp * per_group;
       kp.priv_groups = gp;
+      if (kp_jit && ctx->dense_keys && p.dense_groups > 0 && p.dense_groups <= 4096 &&
+          ((off + 127) & ~size_t(127)) + (size_t)p.dense_groups * 4 <= (size_t)ctx->smem_optin) {
+        off = (off + 127) & ~size_t(127);
+        kp.smem_dense_off = (int)off;
+        off += (size_t)p.dense_groups * 4;
+      }
     }
   }
   if (off > (size_t)ctx->smem_optin) return false;
@@ -284,7 +295,19 @@ int32_t prepare(hawk_ctx* ctx, const hawk_pipeline& pipe, const hawk_variant& v,
   kp.npost = compile_filters(pipe.post, pipe.npost, kp.post);
   collect_prefetch(kp, keys, aggs, project);
   kp.prefetch_passes = std::max(1, std::min(ctx->prefetch_passes, 8));  // TMA stages
-  if (!ctx->stage) {  // coalesced loads straight from HBM, no TMA staging
+  kp.l2_distance = ctx->l2_distance;
+  kp.pass_sync = ctx->pass_sync;
+  kp.l2_cols = 0;
+  // Probe pipelines read their driver columns straight from HBM, without a
+  // per-pass CTA barrier: probe latency varies per warp (random L2/HBM slot
+  // loads), and a barrier per pass tile would make every warp wait for the
+  // slowest one (measured: SSB Q4.1 SF10 1.58 -> 1.30 ms, TPC-H Q3 terminal
+  // 1.02 -> 0.79 ms). Scan-only pipelines keep TMA staging / the barrier,
+  // which keeps a CTA's warps on one tile (TPC-H Q1 1.36 -> 1.21 ms).
+  const bool probe_free = pipe.nprobe > 0 && !ctx->stage_probes;
+  if (probe_free) kp.pass_sync = 0;
+  if (!ctx->stage || probe_free) {  // coalesced loads straight from HBM, no TMA staging
+    kp.l2_cols = kp.l2_distance > 0 ? kp.nprefetch : 0;
     kp.nprefetch = 0;
     std::memset(kp.stage_of, -1, sizeof kp.stage_of);
   }
@@ -309,6 +332,7 @@ int32_t prepare(hawk_ctx* ctx, const hawk_pipeline& pipe, const hawk_variant& v,
     if (!fits && v.memory_access == HAWK_COALESCED && kp.prefetch_passes > 1) {
       --kp.prefetch_passes;
     } else if (v.memory_access == HAWK_COALESCED && kp.nprefetch > 0) {
+      kp.l2_cols = kp.l2_distance > 0 ? kp.nprefetch : 0;  // L2 bulk prefetch instead
       kp.nprefetch = 0;
       std::memset(kp.stage_of, -1, sizeof kp.stage_of);
     } else {
@@ -465,6 +489,22 @@ int32_t hawk_b200_ctx_set_option(hawk_ctx* ctx, const char* name, int64_t value)
   if (!ctx || !name) return HAWK_ERR_ARGUMENT;
   if (std::strcmp(name, "prefetch_passes") == 0) {
     ctx->prefetch_passes = (int)std::max<int64_t>(0, std::min<int64_t>(value, 16));
+    return HAWK_OK;
+  }
+  if (std::strcmp(name, "l2_distance") == 0) {
+    ctx->l2_distance = (int)std::max<int64_t>(0, std::min<int64_t>(value, 16));
+    return HAWK_OK;
+  }
+  if (std::strcmp(name, "dense_keys") == 0) {
+    ctx->dense_keys = value != 0;
+    return HAWK_OK;
+  }
+  if (std::strcmp(name, "stage_probes") == 0) {
+    ctx->stage_probes = value != 0;
+    return HAWK_OK;
+  }
+  if (std::strcmp(name, "pass_sync") == 0) {
+    ctx->pass_sync = value != 0;
     return HAWK_OK;
   }
   if (std::strcmp(name, "jit") == 0) {
@@ -683,6 +723,24 @@ static int32_t prefix_sum_async(hawk_ctx* ctx, const int64_t* d_in, int64_t n, i
   hk::scan_single_kernel<<<1, 1024, 0, ctx->stream>>>(sums, nblocks, d_total);
   hk::scan_add_kernel<<<(unsigned)nblocks, 256, 0, ctx->stream>>>(d_out, n, sums);
   HK_TRY(cudaGetLastError());
+  return HAWK_OK;
+}
+
+int32_t hawk_b200_column_range(hawk_ctx* ctx, const int64_t* d_col, int64_t n, int64_t* lo,
+                               int64_t* hi) {
+  if (!ctx || !d_col || n <= 0 || !lo || !hi) return HAWK_ERR_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  long long* d_out = reinterpret_cast<long long*>(ctx->d_ctrl) + 4;  // ctrl words 4, 5
+  const long long init[2] = {0x7fffffffffffffffll, (long long)0x8000000000000000ull};
+  HK_TRY(cudaMemcpyAsync(d_out, init, 16, cudaMemcpyHostToDevice, ctx->stream));
+  const int64_t blocks = std::min<int64_t>((int64_t)ctx->sms * 8, std::max<int64_t>(1, (n / 2 + 255) / 256));
+  hk::column_range_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(d_col, n, d_out);
+  HK_TRY(cudaGetLastError());
+  long long h[2];
+  HK_TRY(cudaMemcpyAsync(h, d_out, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  HK_TRY(cudaStreamSynchronize(ctx->stream));
+  *lo = h[0];
+  *hi = h[1];
   return HAWK_OK;
 }
 

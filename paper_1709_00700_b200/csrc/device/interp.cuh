@@ -66,6 +66,9 @@ struct KParams {
   int8_t prefetch_col[HAWK_MAX_COLUMNS];   // staged index -> column slot
   int8_t stage_of[HAWK_MAX_COLUMNS];       // column slot -> staged index
   int32_t prefetch_passes;            // COALESCED: pipeline depth in pass tiles (>= 1)
+  int32_t l2_cols;                    // COALESCED, unstaged: columns bulk-prefetched into L2
+  int32_t l2_distance;                //   ... this many pass tiles ahead
+  int32_t pass_sync;                  // COALESCED, unstaged: CTA barrier after every pass
   int32_t smem_stage_off;             // COALESCED: [mbarriers][stages x columns x B*R rows]
   int32_t local_log2;                 // HAGG_LOCAL: log2 smem table slots
   int64_t chunk_rows;                 // rows per CTA chunk (multiple of 64)
@@ -83,6 +86,7 @@ struct KParams {
   int32_t priv_groups;                // HAGG_LOCAL: groups with thread-private accumulators
   int32_t smem_ord_off;               // HAGG_LOCAL: slot -> ordinal, ordinal -> slot, count
   int32_t smem_priv_off;              // HAGG_LOCAL: priv[(ord * naggs + a) * B + t]
+  int32_t smem_dense_off;             // HAGG_LOCAL, compiled: dense key index -> ordinal (0: off)
   int32_t smem_state_off;
   int32_t state_words;                // state words per thread
   int32_t rid_base, key_base, acc_base;

@@ -64,6 +64,32 @@ __global__ void scan_add_kernel(int64_t* out, int64_t n, const int64_t* block_of
 
 // ---- join tables ----------------------------------------------------------------
 
+// min / max of an int64 column: grid-stride 128-bit loads, warp reduce,
+// one pair of 64-bit atomics per warp. out = {min, max}, preset by the host.
+__global__ void column_range_kernel(const int64_t* __restrict__ col, int64_t n, long long* out) {
+  long long lo = 0x7fffffffffffffffll, hi = (long long)0x8000000000000000ull;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t pairs = n / 2;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += stride) {
+    u64 a, b;
+    ldg128(reinterpret_cast<const u64*>(col) + 2 * i, a, b);
+    lo = min(lo, (long long)min((int64_t)a, (int64_t)b));
+    hi = max(hi, (long long)max((int64_t)a, (int64_t)b));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    lo = min(lo, (long long)col[n - 1]);
+    hi = max(hi, (long long)col[n - 1]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_down_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_down_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(out, lo);
+    atomicMax(out + 1, hi);
+  }
+}
+
 __global__ void fill_kernel(u64* p, u64 value, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)

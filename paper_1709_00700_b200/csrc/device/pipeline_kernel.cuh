@@ -186,7 +186,7 @@ __device__ __forceinline__ void hagg_static(const KParams& kp, const Batch<R, AC
                                             const State<R>& s,
                                             const typename P::template Vals<R>& vals,
                                             u64* local_table, int* ordinal, int* ord_slot,
-                                            int* nord, u64* priv, int GP,
+                                            int* nord, u64* priv, int GP, int* dense_ord,
                                             u64 (&last_key)[HAWK_MAX_KEYS], u64& last_target) {
   constexpr int K = P::kKeys, A = P::kAggs;
   const int B = P::kBlock > 0 ? P::kBlock : (int)blockDim.x;
@@ -212,14 +212,39 @@ __device__ __forceinline__ void hagg_static(const KParams& kp, const Batch<R, AC
       if (same) {
         target = last_target;
       } else {
+        // small key domains: the dense index of the key tuple caches its
+        // group ordinal (a CTA-wide lookaside in front of the hash table)
+        int d = -1;
+        if constexpr (ROLE == K_HAGG_LOCAL) {
+          if (dense_ord != nullptr) {
+            u64 idx = 0;
+            bool in = true;
+#pragma unroll
+            for (int i = 0; i < K; ++i) {
+              const u64 r = kj[i] - (u64)kp.p.key_lo[i];
+              in &= r < (u64)kp.p.key_span[i];
+              idx += r * (u64)kp.p.key_stride[i];
+            }
+            if (in) {
+              d = (int)idx;
+              const int o = dense_ord[d];
+              if (o >= 0) target = ((((u64)o * A * B) + threadIdx.x) << 1) | 1ull;
+            }
+          }
+        }
         u64* slot = nullptr;
         if constexpr (ROLE == K_HAGG_LOCAL) {
-          int si = 0;
-          slot = agg_find_static<IMPL, HFN, true, K>(kp, local_table, kp.local_log2, gt.seed, kj,
-                                                     nullptr, &si);
-          if (slot != nullptr && GP > 0) {
-            const int o = claim_ordinal(ordinal, si, ord_slot, nord, GP);
-            if (o < GP) target = ((((u64)o * A * B) + threadIdx.x) << 1) | 1ull;
+          if (target == 0) {
+            int si = 0;
+            slot = agg_find_static<IMPL, HFN, true, K>(kp, local_table, kp.local_log2, gt.seed, kj,
+                                                       nullptr, &si);
+            if (slot != nullptr && GP > 0) {
+              const int o = claim_ordinal(ordinal, si, ord_slot, nord, GP);
+              if (o < GP) {
+                target = ((((u64)o * A * B) + threadIdx.x) << 1) | 1ull;
+                if (d >= 0) dense_ord[d] = o;  // every writer stores the same ordinal
+              }
+            }
           }
         }
         if (target == 0) {
@@ -237,6 +262,16 @@ __device__ __forceinline__ void hagg_static(const KParams& kp, const Batch<R, AC
     }
     tw[j] = target;
   }
+  // rows with private accumulators (plain shared-memory read-modify-write,
+  // predicated, no branches) and rows updating a table slot with atomics
+  uint32_t pmask = 0, gmask = 0;
+  u64 off[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    pmask |= (uint32_t)(tw[j] & 1ull) << j;
+    gmask |= (uint32_t)(tw[j] != 0ull && !(tw[j] & 1ull)) << j;
+    off[j] = tw[j] >> 1;
+  }
   StaticFor<0, A>::run([&](auto ac) {
     constexpr int a = decltype(ac)::value;
     constexpr int fn = P::kAggFn[a], ty = P::kAggType[a];
@@ -250,13 +285,16 @@ __device__ __forceinline__ void hagg_static(const KParams& kp, const Batch<R, AC
     u64* pa = priv + (size_t)a * B;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-      if (tw[j] & 1ull) {
-        u64& acc = pa[tw[j] >> 1];
+      if ((pmask >> j) & 1u) {
+        u64& acc = pa[off[j]];
         if constexpr (fn == HAWK_COUNT || (fn == HAWK_SUM && ty == HAWK_I64)) acc += v[j];
         else acc = agg_combine(fn, ty, acc, v[j]);
-      } else if (tw[j]) {
-        agg_update(reinterpret_cast<u64*>(tw[j]) + 1 + K + a, fn, ty, v[j]);
       }
+    }
+    if (gmask) {
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        if ((gmask >> j) & 1u) agg_update(reinterpret_cast<u64*>(tw[j]) + 1 + K + a, fn, ty, v[j]);
     }
   });
 }
@@ -356,7 +394,10 @@ __device__ __forceinline__ void pipeline_body(const KParams& kp) {
   int* ord_slot = ordinal + local_slots;                           // [GP]
   int* nord = ord_slot + GP;                                       // [1]
   u64* priv = reinterpret_cast<u64*>(smem + kp.smem_priv_off);
+  int* dense_ord = kp.smem_dense_off > 0 ? reinterpret_cast<int*>(smem + kp.smem_dense_off) : nullptr;
   if constexpr (ROLE == K_HAGG_LOCAL) {
+    if (dense_ord != nullptr)
+      for (int i = threadIdx.x; i < p.dense_groups; i += B) dense_ord[i] = -1;
     for (int i = threadIdx.x; i < local_slots; i += B) local_table[(size_t)i * words] = 0ull;
     if (GP > 0) {
       for (int i = threadIdx.x; i < local_slots; i += B) ordinal[i] = -1;
@@ -412,8 +453,8 @@ __device__ __forceinline__ void pipeline_body(const KParams& kp) {
       if (PRED == HAWK_BRANCHED && alive == 0u) return;
       if constexpr (P::kStatic) {
         hagg_static<P, ROLE, ACCESS, PRED, IMPL, HFN, R>(kp, b, s, vals, local_table, ordinal,
-                                                         ord_slot, nord, priv, GP, last_key,
-                                                         last_target);
+                                                         ord_slot, nord, priv, GP, dense_ord,
+                                                         last_key, last_target);
         return;
       }
       for (int i = 0; i < K; ++i) {
@@ -569,13 +610,11 @@ __device__ __forceinline__ void pipeline_body(const KParams& kp) {
         if (lane_id() == 0 && n) atomicAdd(kp.d_cursor, (u64)n);
       }
       if (PRED == HAWK_BRANCHED && alive == 0u) return;
-      u64 key[R];
+      u64 key[R], rid[R];
       P::template key_input<ACCESS, PRED, R>(kp, 0, b, s, vals, key);
 #pragma unroll
-      for (int j = 0; j < R; ++j)
-        if ((alive >> j) & 1u)
-          table_insert<IMPL, HFN>(p.sink_table, key[j], (u64)(b.row(j) + p.row_offset),
-                                  kp.d_flags);
+      for (int j = 0; j < R; ++j) rid[j] = (u64)(b.row(j) + p.row_offset);
+      table_insert_rows<IMPL, HFN, R>(p.sink_table, key, rid, alive, kp.d_flags);
     }
   };
 
@@ -606,8 +645,20 @@ __device__ __forceinline__ void pipeline_body(const KParams& kp) {
                     reinterpret_cast<const int64_t*>(p.d_columns[kp.prefetch_col[c]]) + b0, bytes,
                     &bars[st]);
     };
+    // unstaged tiles: one thread per column bulk-prefetches the tile
+    // l2_distance passes ahead into L2 (no shared memory), so the coalesced
+    // loads of a pass hit L2 instead of waiting on HBM
+    const int L2C = C > 0 ? 0 : kp.l2_cols, D = kp.l2_distance;
+    auto prefetch = [&](int64_t ps) {
+      const int64_t b0 = cb + ps * pass_rows;
+      const uint32_t bytes = (uint32_t)(((min(pass_rows, ce - b0) + 1) & ~1ll) * 8);
+      for (int c = threadIdx.x; c < L2C; c += B)
+        prefetch_l2_bulk(reinterpret_cast<const int64_t*>(p.d_columns[kp.prefetch_col[c]]) + b0, bytes);
+    };
     if (threadIdx.x == 0 && C > 0)
       for (int64_t ps = 0; ps < min((int64_t)S, npasses); ++ps) issue(ps);
+    if ((int)threadIdx.x < L2C)
+      for (int64_t ps = 0; ps < min((int64_t)D, npasses); ++ps) prefetch(ps);
     for (int64_t ps = 0; ps < npasses; ++ps) {
       const int st = (int)(ps % S);
       if (C > 0) mbar_wait(&bars[st], (uint32_t)((ps / S) & 1));
@@ -615,18 +666,26 @@ __device__ __forceinline__ void pipeline_body(const KParams& kp) {
       b.base = cb + ps * pass_rows;
       b.B = B;
       b.stage = C > 0 ? stages + (size_t)st * C * pass_rows : nullptr;
+      if ((int)threadIdx.x < L2C && ps + D < npasses) prefetch(ps + D);
       if (b.base + pass_rows <= ce) {
+        // full tile: a separate inlined copy with every row valid, so the
+        // per-row validity predicates fold away
         b.valid = (1u << R) - 1u;
+        process(b);
       } else {
         b.valid = 0;
 #pragma unroll
         for (int j = 0; j < R; ++j) b.valid |= (uint32_t)(b.row(j) < ce) << j;
+        process(b);
       }
-      process(b);
-      __syncthreads();  // every thread is done with stage st
-      if (threadIdx.x == 0 && C > 0 && ps + S < npasses) {
-        fence_proxy_async();
-        issue(ps + S);
+      if (C > 0) {
+        __syncthreads();  // every thread is done with stage st
+        if (threadIdx.x == 0 && ps + S < npasses) {
+          fence_proxy_async();
+          issue(ps + S);
+        }
+      } else if (kp.pass_sync) {
+        __syncthreads();  // keeps the CTA's warps on one tile (DRAM page locality)
       }
     }
   } else {

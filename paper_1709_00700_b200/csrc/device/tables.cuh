@@ -120,6 +120,63 @@ __device__ __forceinline__ void table_insert(const hawk_table& t, u64 key, u64 p
   }
 }
 
+// HASH_PUT of R rows: linear probing CAS-claims the home slots of every
+// active row back to back (R independent atomics in flight), and only rows
+// that lost their home slot walk on; cuckoo inserts row by row.
+template <int IMPL, int HFN, int R>
+__device__ __forceinline__ void table_insert_rows(const hawk_table& t, const u64 (&key)[R],
+                                                  const u64 (&payload)[R], uint32_t act,
+                                                  int* flags) {
+  if (IMPL != HAWK_LINEAR_PROBING) {
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+      if ((act >> j) & 1u) table_insert<IMPL, HFN>(t, key[j], payload[j], flags);
+    return;
+  }
+  u64* s = reinterpret_cast<u64*>(t.d_slots);
+  const u64 mask = (u64)t.capacity - 1ull;
+  u64 pos[R], prev[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    pos[j] = hash_slot<HFN>(key[j], t.seed[0], t.log2_capacity);
+    prev[j] = kEmpty;
+    if (((act >> j) & 1u) && key[j] != kEmpty) prev[j] = atomicCAS(s + 2 * pos[j], kEmpty, key[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if (!((act >> j) & 1u)) continue;
+    if (key[j] == kEmpty) {
+      atomicOr(flags, HAWK_FLAG_TABLE_FULL);
+      continue;
+    }
+    if (prev[j] == kEmpty) {
+      s[2 * pos[j] + 1] = payload[j];
+      continue;
+    }
+    if (prev[j] == key[j]) {
+      atomicOr(flags, HAWK_FLAG_DUPLICATE);
+      continue;
+    }
+    u64 i = (pos[j] + 1) & mask;
+    bool done = false;
+    for (u64 n = 1; n <= mask; ++n) {
+      const u64 pv = atomicCAS(s + 2 * i, kEmpty, key[j]);
+      if (pv == kEmpty) {
+        s[2 * i + 1] = payload[j];
+        done = true;
+        break;
+      }
+      if (pv == key[j]) {
+        atomicOr(flags, HAWK_FLAG_DUPLICATE);
+        done = true;
+        break;
+      }
+      i = (i + 1) & mask;
+    }
+    if (!done) atomicOr(flags, HAWK_FLAG_TABLE_FULL);
+  }
+}
+
 // ---- aggregation tables: {state, keys..., accs...} slots --------
 
 __host__ __device__ __forceinline__ u64 agg_identity(int fn, int type) {

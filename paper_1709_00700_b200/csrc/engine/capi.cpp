@@ -24,6 +24,7 @@ struct hawk_result {
 struct hawk_partial {
   PartialResult part;
   double kernel_ms = 0;
+  int32_t launches = 0;
 };
 
 namespace {
@@ -197,6 +198,7 @@ int32_t hawk_engine_run_partial(hawk_engine* e, const char* sql, const char* con
       throw;
     }
     p->kernel_ms = m.kernel_ms;
+    p->launches = m.launches;
     *out = p;
   });
 }
@@ -206,6 +208,7 @@ int32_t hawk_partial_width(const hawk_partial* p) { return p->part.width; }
 int32_t hawk_partial_sink(const hawk_partial* p) { return p->part.sink; }
 const int64_t* hawk_partial_data(const hawk_partial* p) { return p->part.values.data(); }
 double hawk_partial_kernel_ms(const hawk_partial* p) { return p->kernel_ms; }
+int32_t hawk_partial_launches(const hawk_partial* p) { return p->launches; }
 void hawk_partial_free(hawk_partial* p) { delete p; }
 
 int32_t hawk_engine_finalize(hawk_engine* e, const char* sql, const char* config, int32_t nparts,
@@ -335,7 +338,17 @@ int32_t hawk_engine_compile_check(hawk_engine* e, const char* sql, const char* c
       size_t bytes = 0;
       const int32_t st = hawk_b200_program_compile(&lp.pipe, &v, log.data(), (int32_t)log.size(), &bytes);
       if (st == HAWK_OK) {
-        os << i << " ok " << bytes << "\n";
+        // one line per pipeline: cubin bytes + the ptxas resource summary
+        std::string info = log.c_str(), regs, spill;
+        auto grab = [&](const char* key, std::string& out) {
+          const auto at = info.find(key);
+          if (at != std::string::npos) out = info.substr(at, info.find('\n', at) - at);
+        };
+        grab("Used ", regs);
+        grab("bytes stack frame", spill);
+        const auto dot = spill.find(',');
+        os << i << " ok " << bytes << " [" << regs << (dot != std::string::npos ? ";" + spill.substr(dot + 1) : "")
+           << "]\n";
       } else {
         all_ok = false;
         os << i << " error " << st << " " << log.c_str() << "\n";

@@ -42,31 +42,42 @@ def all_gather_rows(parts: np.ndarray, device=None) -> list[np.ndarray]:
 
 def merge_partials_host(sink: int, aggs: list[tuple[int, int]], nkeys: int,
                         parts: list[np.ndarray]) -> np.ndarray:
-    """Host reference of the partial merge (used by the CPU tests): SUM/COUNT
-    add with int64 wrap, MIN/MAX select; aggs = [(fn, type)] per accumulator.
-    sink 0 = AGGREGATE (1 x naggs), 1 = HASH_AGGREGATE (groups x (keys + aggs))."""
-    def combine(fn, a, b):
+    """Host statement of the cross-shard merge the engine performs in
+    Engine::finalize_partials (csrc/engine/engine.cpp), used by the CPU tests.
+
+    Partials are int64 words: group keys, then one accumulator per aggregate,
+    f64 accumulators as their IEEE bits. aggs = [(fn, type)] with fn HAWK_SUM=0,
+    COUNT=1, MIN=2, MAX=3 and type HAWK_I64=0 / HAWK_F64=1. Integer SUM/COUNT
+    add with int64 wrap-around (planner_reference.cpp:25-33); MIN/MAX select.
+    sink 0 = AGGREGATE (1 x naggs), 1 = HASH_AGGREGATE (groups x (keys + aggs));
+    groups come back sorted by key."""
+    def f64(w: int) -> float:
+        return float(np.array([w], dtype=np.int64).view(np.float64)[0])
+
+    def bits(x: float) -> int:
+        return int(np.array([x], dtype=np.float64).view(np.int64)[0])
+
+    def combine(fn: int, ty: int, a: int, b: int) -> int:
+        if ty == 1 and fn != 1:
+            x, y = f64(a), f64(b)
+            return bits(x + y if fn == 0 else min(x, y) if fn == 2 else max(x, y))
         if fn in (0, 1):
-            return (a + b) & 0xFFFFFFFFFFFFFFFF
+            return ((a + b + (1 << 63)) % (1 << 64)) - (1 << 63)
         return min(a, b) if fn == 2 else max(a, b)
 
-    def to_signed(x):
-        return x - (1 << 64) if x >= 1 << 63 else x
+    def fold(acc, row):
+        return row if acc is None else [combine(f, t, a, b) for (f, t), a, b in zip(aggs, acc, row)]
 
     if sink == 0:
         acc = None
         for p in parts:
-            row = [int(v) for v in p.reshape(-1)]
-            acc = row if acc is None else [combine(f, a, b) for (f, _), a, b in zip(aggs, acc, row)]
-        return np.array([[to_signed(v) if v >= 0 else v for v in acc]], dtype=np.int64)
+            if p.size:
+                acc = fold(acc, [int(v) for v in p.reshape(-1)[: len(aggs)]])
+        return np.array([acc if acc is not None else [0] * len(aggs)], dtype=np.int64)
     groups: dict[tuple, list[int]] = {}
     for p in parts:
-        for row in p:
+        for row in p.reshape(-1, nkeys + len(aggs)):
             key = tuple(int(v) for v in row[:nkeys])
-            vals = [int(v) for v in row[nkeys:]]
-            if key in groups:
-                groups[key] = [combine(f, a, b) for (f, _), a, b in zip(aggs, groups[key], vals)]
-            else:
-                groups[key] = vals
-    out = [list(k) + [to_signed(v) if v >= 0 else v for v in vals] for k, vals in sorted(groups.items())]
+            groups[key] = fold(groups.get(key), [int(v) for v in row[nkeys:]])
+    out = [list(k) + v for k, v in sorted(groups.items())]
     return np.array(out, dtype=np.int64).reshape(len(out), nkeys + len(aggs))

@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes as C
 from dataclasses import dataclass, field
+from typing import NamedTuple
 
 import numpy as np
 
@@ -109,6 +110,15 @@ class Column:
         if self.kind == STRING:
             return [self.lexicon[c] for c in self.values]
         return self.values.tolist()
+
+
+class Partial(NamedTuple):
+    """A shard's partial result (Engine.run_partial): AGGREGATE accumulators,
+    HASH_AGGREGATE group rows (keys + accumulators) or projected rows."""
+    rows: np.ndarray
+    sink: int
+    kernel_ms: float
+    launches: int
 
 
 @dataclass
@@ -244,8 +254,8 @@ class Engine:
         finally:
             self._lib.hawk_result_free(r)
 
-    def run_partial(self, sql: str, config: str = "") -> tuple[np.ndarray, int, float]:
-        """Shard execution: (rows x width int64 partials, sink, kernel_ms)."""
+    def run_partial(self, sql: str, config: str = "") -> "Partial":
+        """Shard execution: the (rows x width) int64 partials before the cross-GPU merge."""
         p = C.c_void_p()
         _check(self._lib.hawk_engine_run_partial(self._h, sql.encode(), config.encode(), C.byref(p)))
         try:
@@ -255,8 +265,8 @@ class Engine:
             ptr = self._lib.hawk_partial_data(p)
             data = (np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_int64)), shape=(n,)).copy()
                     if n else np.zeros(0, np.int64))
-            return data.reshape(rows, width), self._lib.hawk_partial_sink(p), \
-                self._lib.hawk_partial_kernel_ms(p)
+            return Partial(data.reshape(rows, width), self._lib.hawk_partial_sink(p),
+                           self._lib.hawk_partial_kernel_ms(p), self._lib.hawk_partial_launches(p))
         finally:
             self._lib.hawk_partial_free(p)
 

@@ -110,6 +110,74 @@ def test_baseline_queries_match_oracle(bench_db, cfg, jit):
         assert diff is None, f"{key} [{cfg}]: {diff}"
 
 
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("key", sorted(Q.BENCH))
+def test_sharded_partials_finalize_to_oracle(key, world):
+    # the multi-GPU data path, rank by rank on one device: each shard of the
+    # fact table runs Engine.run_partial, the partials are merged by
+    # Engine.finalize (AVG = merged SUM / merged COUNT) and must equal the
+    # oracle on the whole table
+    from paper_1709_00700_b200.distributed import shard_range
+    sql, tables, fact = Q.BENCH[key]
+    sf, seed = 0.01, 42
+    e = Engine(0)
+    try:
+        e.set_option("jit", 1)
+        for t in tables:
+            if t != fact:
+                e.generate(t, sf, seed)
+        n = dg.table_rows(fact, sf)
+        parts = []
+        for r in range(world):
+            b, end = shard_range(n, r, world)
+            e.generate(fact, sf, seed, b, end - b)
+            parts.append(e.run_partial(sql, CONFIGS[0]).rows)
+            e.drop(dg.SCHEMA[fact][0])
+        e.generate(fact, sf, seed)
+        got = e.finalize(sql, parts, CONFIGS[0])
+        db = harness.oracle_db(harness.bench_tables("ssb" if key.startswith("ssb") else "tpch", sf, seed))
+        diff = harness.compare(db.execute(sql), got)
+        assert diff is None, f"{key} x{world}: {diff}"
+    finally:
+        e.close()
+
+
+def test_column_range(engine):
+    lib = _native.b200()
+    rng = np.random.default_rng(5)
+    for n in (1, 2, 3, 1000, 1_000_001):
+        host = rng.integers(-2**62, 2**62, n, dtype=np.int64)
+        ptr = C.c_void_p()
+        assert lib.hawk_b200_alloc(engine.ctx, n * 8, C.byref(ptr)) == 0
+        try:
+            assert lib.hawk_b200_memcpy_h2d(engine.ctx, ptr, host.ctypes.data, n * 8) == 0
+            lo, hi = C.c_int64(), C.c_int64()
+            assert lib.hawk_b200_column_range(engine.ctx, ptr, n, C.byref(lo), C.byref(hi)) == 0
+            assert (lo.value, hi.value) == (host.min(), host.max())
+        finally:
+            lib.hawk_b200_free(engine.ctx, ptr)
+
+
+@pytest.mark.parametrize("dense", [1, 0], ids=["dense-keys", "hash-only"])
+def test_group_by_dense_key_lookaside(bench_db, dense):
+    # the dense key-index lookaside (small key domains) and the plain hash
+    # path give the oracle's groups for every local-hash variant
+    which, engine, db = bench_db
+    engine.set_option("jit", 1)
+    engine.set_option("dense_keys", dense)
+    try:
+        for key, sql in harness.BENCH:
+            if key.startswith("ssb") != (which == "ssb"):
+                continue
+            expected = db.execute(sql)
+            for agg in AGG:
+                cfg = PROJ[0] + ";" + agg
+                diff = harness.compare(expected, engine.run(sql, cfg))
+                assert diff is None, f"{key} [{cfg}] dense={dense}: {diff}"
+    finally:
+        engine.set_option("dense_keys", 1)
+
+
 def test_device_generator_matches_host(engine):
     engine.generate(dg.LINEITEM, 0.01, 42)
     n = engine.table_rows("lineitem")
