@@ -105,6 +105,22 @@ struct ExecutionMetrics {
   std::vector<PipelineMetrics> pipelines;
 };
 
+/// A query result as plain columns (the C ABI's result form). Strings are
+/// codes into `lexicon` in first-appearance order, as a reference Table
+/// encodes them (storage_table.cpp:127-135); to_table() builds that Table.
+struct ResultColumn {
+  std::string name;
+  ColumnKind kind = ColumnKind::Int64;
+  std::vector<int64_t> ints;   // Int64 values / String codes
+  std::vector<double> floats;  // Float64 values
+  std::vector<std::string> lexicon;
+};
+struct ResultColumns {
+  std::vector<ResultColumn> columns;
+  int64_t rows = 0;
+  Table to_table() const;
+};
+
 /// Partial result of a fact-table shard, before the cross-GPU merge.
 struct PartialResult {
   int sink = HAWK_SINK_AGGREGATE;
@@ -150,6 +166,10 @@ class Engine {
   /// hash choice is propagated to the build descriptors (ir/passes.hpp:23-26).
   Table execute(const PipelineSet& set, const WorkloadConfig& config,
                 ExecutionMetrics* metrics = nullptr);
+  /// execute() returning plain columns: skips building the reference Table
+  /// (whose finalize() hashes every column for its distinct counts).
+  ResultColumns execute_columns(const PipelineSet& set, const std::vector<VariantConfiguration>& configs,
+                                ExecutionMetrics* metrics = nullptr);
   /// Parses, partitions and executes a SQL query against the device store.
   Table run_sql(const std::string& sql, const WorkloadConfig& config,
                 ExecutionMetrics* metrics = nullptr);
@@ -161,6 +181,10 @@ class Engine {
   /// Merges partials gathered from all shards and finalises the result Table.
   Table finalize_partials(const PipelineSet& set, const WorkloadConfig& config,
                           const std::vector<PartialResult>& parts);
+  ResultColumns finalize_partials_columns(const PipelineSet& set, const WorkloadConfig& config,
+                                          const std::vector<PartialResult>& parts);
+  /// Bumped by every change to the device store (plan caches key on it).
+  uint64_t catalog_generation() const { return generation_; }
 
   /// Flushes L2 (timing hygiene).
   void flush_l2();
@@ -170,6 +194,7 @@ class Engine {
  private:
   std::unique_ptr<Impl> impl_;
   int device_ = 0;
+  uint64_t generation_ = 0;
   hawk_ctx* ctx_ = nullptr;
 };
 

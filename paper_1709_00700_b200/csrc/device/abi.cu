@@ -2,6 +2,7 @@
 // contexts, HBM arena calls, and execute_kernel_plan for
 // one lowered pipeline: strategy -> kernel roles, launch shapes, shared-memory
 // layout, multi-pass orchestration, result/flag read-back.
+#include <chrono>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -27,6 +28,7 @@ struct hawk_ctx {
   int pass_sync = 1;        // COALESCED, unstaged: CTA barrier after every pass tile
   int stage_probes = 0;     // COALESCED pipelines with probes: TMA staging + barrier too
   int dense_keys = 1;       // HAGG_LOCAL compiled: dense key-index lookaside when provided
+  int compact = 1;          // compiled, branched: compact live rows after the first probe
   int priv_groups = 64;     // HAGG_LOCAL: groups with thread-private accumulators
   int jit = 0;              // compiled programs (jit.cu) instead of the interpreter
   int stage = 1;            // COALESCED: stage pass tiles in smem with TMA
@@ -249,6 +251,12 @@ bool layout_smem(hawk_ctx* ctx, hk::KParams& kp, int role, int access, int impl,
       }
     }
   }
+  kp.smem_queue_off = 0;
+  if (kp_jit && kp.split) {  // per-warp queues of compacted rows: 32 * R entries of 8 B
+    off = (off + 127) & ~size_t(127);
+    kp.smem_queue_off = (int)off;
+    off += (size_t)((block + 31) / 32) * 32 * R * 8;
+  }
   if (off > (size_t)ctx->smem_optin) return false;
   *smem_out = off;
   return true;
@@ -284,6 +292,15 @@ int32_t occupancy(int role, const hawk_variant& v, int block, size_t smem, int* 
   return cuda_status(e);
 }
 
+// compiled, branched programs with a probe compact their live rows after it
+// (worth it when work follows the first probe: more probes or a group-by;
+// SSB Q1.1's single probe + SUM gains nothing)
+bool split_rows_for(const hawk_pipeline& pipe, const hawk_variant& v, int role) {
+  return v.predication == HAWK_BRANCHED && pipe.nprobe >= 1 &&
+         (pipe.nprobe >= 2 || role == hk::K_HAGG_LOCAL || role == hk::K_HAGG_GLOBAL) &&
+         (role <= hk::K_HAGG_GLOBAL || role == hk::K_PROJECT_SINGLE);
+}
+
 int32_t prepare(hawk_ctx* ctx, const hawk_pipeline& pipe, const hawk_variant& v, int role,
                 int block, int64_t grid_or_zero, int64_t per_sm_cap, hk::KParams& kp,
                 hk::LaunchShape& shape) {
@@ -312,6 +329,9 @@ int32_t prepare(hawk_ctx* ctx, const hawk_pipeline& pipe, const hawk_variant& v,
     std::memset(kp.stage_of, -1, sizeof kp.stage_of);
   }
   block = std::min(block, hk::kMaxBlock);
+  // live-row compaction after the first probe (compiled, branched; the
+  // multi-pass roles need CTA-uniform control flow and keep the R-row path)
+  kp.split = ctx->jit && ctx->compact && split_rows_for(pipe, v, role);
   shape.jit_fn = nullptr;
   if (ctx->jit) {  // compiled program: generate + NVRTC (cached), see jit.cu
     std::string err;
@@ -451,9 +471,10 @@ static int main_role(const hawk_pipeline& p, const hawk_variant& v) {
   }
 }
 
-static void program_params(const hawk_pipeline& p, hk::KParams& kp) {
+static void program_params(const hawk_pipeline& p, const hawk_variant& v, hk::KParams& kp) {
   std::memset(&kp, 0, sizeof kp);
   kp.p = p;
+  kp.split = split_rows_for(p, v, main_role(p, v));  // the default context options
   kp.npre = compile_filters(p.filter, p.nfilter, kp.pre);
   kp.npost = compile_filters(p.post, p.npost, kp.post);
 }
@@ -462,7 +483,7 @@ int32_t hawk_b200_program_source(const hawk_pipeline* p, const hawk_variant* v, 
                                  int32_t len) {
   if (!p || !v || !buf || len <= 0) return HAWK_ERR_ARGUMENT;
   hk::KParams kp;
-  program_params(*p, kp);
+  program_params(*p, *v, kp);
   const std::string s = hk::jit_source(kp, main_role(*p, *v), *v);
   std::strncpy(buf, s.c_str(), (size_t)len - 1);
   buf[len - 1] = 0;
@@ -473,7 +494,7 @@ int32_t hawk_b200_program_compile(const hawk_pipeline* p, const hawk_variant* v,
                                   int32_t len, size_t* cubin_bytes) {
   if (!p || !v) return HAWK_ERR_ARGUMENT;
   hk::KParams kp;
-  program_params(*p, kp);
+  program_params(*p, *v, kp);
   std::string err;
   size_t n = 0;
   const int32_t st = hk::jit_compile_only(kp, main_role(*p, *v), *v, &n, &err);
@@ -493,6 +514,10 @@ int32_t hawk_b200_ctx_set_option(hawk_ctx* ctx, const char* name, int64_t value)
   }
   if (std::strcmp(name, "l2_distance") == 0) {
     ctx->l2_distance = (int)std::max<int64_t>(0, std::min<int64_t>(value, 16));
+    return HAWK_OK;
+  }
+  if (std::strcmp(name, "compact") == 0) {
+    ctx->compact = value != 0;
     return HAWK_OK;
   }
   if (std::strcmp(name, "dense_keys") == 0) {
@@ -565,10 +590,14 @@ int32_t hawk_b200_flush_l2(hawk_ctx* ctx) {
   if (!ctx->d_flush || ctx->flush_bytes < want) {
     if (ctx->d_flush) cudaFree(ctx->d_flush);
     HK_TRY(cudaMalloc(&ctx->d_flush, want));
+    HK_TRY(cudaMemset(ctx->d_flush, 0, want));
+    HK_TRY(cudaDeviceSynchronize());
     ctx->flush_bytes = want;
   }
-  static int salt = 0;
-  HK_TRY(cudaMemsetAsync(ctx->d_flush, (++salt) & 0xff, ctx->flush_bytes, ctx->stream));
+  hk::flush_read_kernel<<<ctx->sms * 8, 256, 0, ctx->stream>>>(
+      reinterpret_cast<const hk::u64*>(ctx->d_flush), (int64_t)(ctx->flush_bytes / 16),
+      reinterpret_cast<hk::u64*>(ctx->d_ctrl) + 6);
+  HK_TRY(cudaGetLastError());
   return HAWK_OK;
 }
 
@@ -903,6 +932,11 @@ int32_t hawk_b200_run_pipeline(hawk_ctx* ctx, const hawk_pipeline* pipe, const h
   hk::LaunchShape shape{}, count_shape{};
   int role = -1;
   int64_t out_stride = 0;
+  const bool trace = std::getenv("HAWK_TRACE") != nullptr;
+  auto t_start = std::chrono::steady_clock::now();
+  auto us_since = [&](std::chrono::steady_clock::time_point t) {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t).count();
+  };
   if (aggregation) {
     const bool local = s == HAWK_LOCAL_HASH;
     const bool grouped = p.sink == HAWK_SINK_HASH_AGGREGATE;
@@ -972,6 +1006,7 @@ int32_t hawk_b200_run_pipeline(hawk_ctx* ctx, const hawk_pipeline* pipe, const h
     return HAWK_ERR_INVALID_CONFIG;
   }
 
+  const double t_prepare = trace ? us_since(t_start) : 0.0;
   HK_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
   int nlaunch = 0;
   if (s == HAWK_MULTI_PASS) {
@@ -1006,11 +1041,15 @@ int32_t hawk_b200_run_pipeline(hawk_ctx* ctx, const hawk_pipeline* pipe, const h
     if (st != HAWK_OK) return st;
   }
   HK_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
+  const double t_launch = trace ? us_since(t_start) : 0.0;
   u64 ctrl[4];
   HK_TRY(cudaMemcpyAsync(ctrl, ctx->d_ctrl, sizeof ctrl, cudaMemcpyDeviceToHost, ctx->stream));
   HK_TRY(cudaStreamSynchronize(ctx->stream));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  if (trace)
+    std::fprintf(stderr, "[hawk]   run_pipeline: prepare %.1f us, launched %.1f us, done %.1f us (kernels %.1f us)\n",
+                 t_prepare, t_launch, us_since(t_start), ms * 1e3);
 
   std::memset(out, 0, sizeof *out);
   out->flags = (int32_t)(ctrl[0] & 0xffffffffu);

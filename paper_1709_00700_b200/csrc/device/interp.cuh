@@ -87,6 +87,8 @@ struct KParams {
   int32_t smem_ord_off;               // HAGG_LOCAL: slot -> ordinal, ordinal -> slot, count
   int32_t smem_priv_off;              // HAGG_LOCAL: priv[(ord * naggs + a) * B + t]
   int32_t smem_dense_off;             // HAGG_LOCAL, compiled: dense key index -> ordinal (0: off)
+  int32_t split;                      // compiled, branched: compact live rows after the first probe
+  int32_t smem_queue_off;             //   ... per-warp queues of (row, probe-0 row id)
   int32_t smem_state_off;
   int32_t state_words;                // state words per thread
   int32_t rid_base, key_base, acc_base;
@@ -97,14 +99,20 @@ struct KParams {
 //   TMA bulk copies; thread t owns tile rows t + jB (conflict-free LDS).
 // SEQUENTIAL: thread t owns rows base + j of its own sub-chunk, read from
 //   HBM with 128-bit loads (rows come in aligned pairs).
+// kGather: R explicit rows (the compacted rows of a warp after the first
+// probe; compiled programs only).
+constexpr int kGather = 7;
 template <int R, int ACCESS>
 struct Batch {
+  static constexpr int kR = R, kAccess = ACCESS;
   int64_t base;
   int B;
   uint32_t valid;          // rows inside the CTA chunk
   const int64_t* stage;    // COALESCED: this pass's staged tile
+  int64_t rows_[ACCESS == kGather ? R : 1];
   __device__ __forceinline__ int sidx(int j) const { return threadIdx.x + j * B; }
   __device__ __forceinline__ int64_t row(int j) const {
+    if constexpr (ACCESS == kGather) return rows_[j];
     if (ACCESS == HAWK_COALESCED) return base + sidx(j);
     return base + j;
   }
@@ -131,7 +139,10 @@ template <int R, int ACCESS>
 __device__ __forceinline__ void load_column(const KParams& kp, int slot, const Batch<R, ACCESS>& b,
                                             u64 (&v)[R]) {
   const int64_t* __restrict__ c = reinterpret_cast<const int64_t*>(kp.p.d_columns[slot]);
-  if (ACCESS == HAWK_COALESCED) {
+  if constexpr (ACCESS == kGather) {  // compacted rows: gathers
+#pragma unroll
+    for (int j = 0; j < R; ++j) v[j] = ((b.valid >> j) & 1u) ? ldg64(c + b.row(j)) : 0ull;
+  } else if constexpr (ACCESS == HAWK_COALESCED) {
     if (b.stage) {  // staged tile in shared memory
       const int64_t* t = b.stage + (size_t)kp.stage_of[slot] * b.B * R;
 #pragma unroll
@@ -140,9 +151,7 @@ __device__ __forceinline__ void load_column(const KParams& kp, int slot, const B
 #pragma unroll
       for (int j = 0; j < R; ++j) v[j] = ((b.valid >> j) & 1u) ? ldg64(c + b.row(j)) : 0ull;
     }
-    return;
-  }
-  if (b.valid == (1u << R) - 1u) {
+  } else if (b.valid == (1u << R) - 1u) {
 #pragma unroll
     for (int j = 0; j < R; j += 2) ldg128(c + b.row(j), v[j], v[j + 1]);
   } else {

@@ -90,6 +90,20 @@ __global__ void column_range_kernel(const int64_t* __restrict__ col, int64_t n, 
   }
 }
 
+// L2 flush by reading a buffer twice the L2 size: evicts the working set
+// while leaving only clean lines behind (a memset flush leaves dirty lines
+// whose write-back would land in the next timed kernel).
+__global__ void flush_read_kernel(const u64* __restrict__ p, int64_t pairs, u64* sink) {
+  u64 acc = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += stride) {
+    u64 a, b;
+    ldg128(p + 2 * i, a, b);
+    acc ^= a ^ b;
+  }
+  if (acc == 0x9e3779b97f4a7c15ull) *sink = acc;  // never true for a zeroed buffer; keeps the loads
+}
+
 __global__ void fill_kernel(u64* p, u64 value, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)

@@ -67,6 +67,7 @@ __device__ __forceinline__ void evaluate(const KParams& kp, const Batch<R, ACCES
 // inlined and per-row values in registers.
 struct InterpProg {
   static constexpr bool kStatic = false;  // program shape known only at run time
+  static constexpr bool kSplit = false;   // no live-row compaction after the first probe
   static constexpr int kBlock = 0;        // block size known only at run time
   template <int R>
   struct Vals {};
@@ -354,6 +355,102 @@ __device__ __forceinline__ u64 block_exclusive_scan(u64 v, u64* scratch, u64& to
 }
 
 
+template <class T>
+struct Plain {
+  using type = T;
+};
+template <class T>
+struct Plain<T&> {
+  using type = T;
+};
+template <class T>
+struct Plain<const T> {
+  using type = T;
+};
+template <class T>
+struct Plain<const T&> {
+  using type = T;
+};
+
+// PROJECT, single pass (compiled programs): warp-aggregated atomic cursor
+template <class P, int ACCESS, int PRED, int R>
+__device__ __forceinline__ void project_static(const KParams& kp, const Batch<R, ACCESS>& b,
+                                               const State<R>& s,
+                                               const typename P::template Vals<R>& vals) {
+  const uint32_t alive = s.alive;
+  const unsigned mask = warp_mask();
+  const int last = warp_size_here() - 1;
+  const uint32_t cnt = (uint32_t)__popc(alive);
+  const uint32_t incl = warp_incl_scan<uint32_t>(cnt, mask);
+  const uint32_t tot = __shfl_sync(mask, incl, last);
+  u64 base = 0;
+  if (lane_id() == last && tot) base = atomicAdd(kp.d_cursor, (u64)tot);
+  base = __shfl_sync(mask, base, last);
+  if (cnt) {
+    const u64 pos = base + incl - cnt;
+    for (int i = 0; i < kp.p.nproject; ++i) {
+      u64 v[R];
+      P::template proj_input<ACCESS, PRED, R>(kp, i, b, s, vals, v);
+      int64_t* out = kp.d_out + (size_t)i * kp.out_stride + pos;
+      int k = 0;
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        if ((alive >> j) & 1u) out[k++] = (int64_t)v[j];
+    }
+  }
+}
+
+// Live-row compaction (compiled, branched): the filters and the first (most
+// selective) probe run on the pass's R rows per thread; the surviving rows of
+// the warp are packed into a per-warp queue (row, probe-0 row id) and the rest
+// of the chain + the sink run on them one row per lane, so the later probes
+// issue instructions for live rows only (SSB Q4.1: 20% of the rows survive the
+// first probe). The compiled eval2 loads every driver column it and the sink
+// need at its start, so the gathers overlap instead of forming a chain of HBM
+// round trips between the probes.
+template <class P, int ROLE, int ACCESS, int PRED, int IMPL, int HFN, int R, class Sink>
+__device__ __forceinline__ void split_rows(const KParams& kp, const Batch<R, ACCESS>& b,
+                                           State<R>& s, typename P::template Vals<R>& vals,
+                                           int64_t cb, int B, unsigned char* smem, Sink& sink) {
+  P::template eval1<ACCESS, PRED, IMPL, HFN, R>(kp, b, s, vals);
+  const uint32_t alive = s.alive;
+  const unsigned mask = warp_mask();
+  const int last = warp_size_here() - 1;
+  const uint32_t c = (uint32_t)__popc(alive);
+  const uint32_t incl = warp_incl_scan<uint32_t>(c, mask);
+  const uint32_t total = __shfl_sync(mask, incl, last);
+  if (total == 0u) return;
+  uint2* q = reinterpret_cast<uint2*>(smem + kp.smem_queue_off) + (threadIdx.x >> 5) * (32 * R);
+  uint32_t pos = incl - c;
+#pragma unroll
+  for (int j = 0; j < R; ++j)
+    if ((alive >> j) & 1u) q[pos++] = make_uint2((uint32_t)(b.row(j) - cb), (uint32_t)vals.p0[j]);
+  __syncwarp(mask);
+  for (uint32_t it = 0; it < total; it += 32u) {
+    const uint32_t idx = it + (uint32_t)lane_id();
+    Batch<1, kGather> g;
+    g.base = cb;
+    g.B = B;
+    g.stage = nullptr;
+    g.valid = idx < total ? 1u : 0u;
+    const uint2 e = g.valid ? q[idx] : make_uint2(0u, 0u);
+    g.rows_[0] = cb + (int64_t)e.x;
+    typename P::template Vals<1> v1;
+    v1.p0[0] = (int32_t)e.y;
+    State<1> s1;
+    s1.ts = s.ts;
+    s1.B = s.B;
+    s1.tid = s.tid;
+    s1.rid_base = s.rid_base;
+    s1.key_base = s.key_base;
+    s1.acc_base = s.acc_base;
+    s1.alive = g.valid;
+    P::template eval2<kGather, PRED, IMPL, HFN, 1>(kp, g, s1, v1);
+    sink(g, s1, v1);
+  }
+  __syncwarp(mask);
+}
+
 template <class P, int ROLE, int ACCESS, int PRED, int IMPL, int HFN, int U>
 __device__ __forceinline__ void pipeline_body(const KParams& kp) {
   constexpr int R = 4 * U;
@@ -413,7 +510,28 @@ __device__ __forceinline__ void pipeline_body(const KParams& kp) {
   u64 last_key[HAWK_MAX_KEYS] = {0, 0, 0, 0};  // HAGG: the thread's last group
   u64 last_target = 0;
 
+  // sinks of compiled programs for any batch shape (R rows / compacted rows)
+  auto sink_static = [&](const auto& bb, auto& ss, auto& vv) {
+    using BT = typename Plain<decltype(bb)>::type;
+    constexpr int RR = BT::kR, AA = BT::kAccess;
+    if constexpr (ROLE == K_AGG_LOCAL || ROLE == K_AGG_GLOBAL) {
+      if (ss.alive == 0u) return;
+      agg_static<P, AA, PRED, RR>(kp, bb, ss, vv);
+    } else if constexpr (ROLE == K_HAGG_LOCAL || ROLE == K_HAGG_GLOBAL) {
+      if (ss.alive == 0u) return;
+      hagg_static<P, ROLE, AA, PRED, IMPL, HFN, RR>(kp, bb, ss, vv, local_table, ordinal, ord_slot,
+                                                    nord, priv, GP, dense_ord, last_key,
+                                                    last_target);
+    } else if constexpr (ROLE == K_PROJECT_SINGLE) {
+      project_static<P, AA, PRED, RR>(kp, bb, ss, vv);
+    }
+  };
   auto process = [&](const Batch<R, ACCESS>& b) {
+    if constexpr (P::kSplit && PRED == HAWK_BRANCHED &&
+                  (ROLE <= K_HAGG_GLOBAL || ROLE == K_PROJECT_SINGLE)) {
+      split_rows<P, ROLE, ACCESS, PRED, IMPL, HFN, R>(kp, b, s, vals, cb, B, smem, sink_static);
+      return;
+    }
     P::template eval<ACCESS, PRED, IMPL, HFN, R>(kp, b, s, vals);
     const uint32_t alive = s.alive;
     if constexpr (ROLE == K_AGG_LOCAL || ROLE == K_AGG_GLOBAL) {

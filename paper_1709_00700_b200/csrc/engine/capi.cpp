@@ -2,6 +2,7 @@
 // No exception crosses this boundary: each is mapped to its hawk_status class.
 #include <cstring>
 #include <sstream>
+#include <unordered_map>
 
 #include "hawk/sql/parser.hpp"
 #include "hawk_b200_engine.h"
@@ -12,11 +13,14 @@ using namespace hawk::b200;
 
 struct hawk_engine {
   Engine engine;
+  // parsed + partitioned plans by SQL text, valid for one catalog generation
+  std::unordered_map<std::string, PipelineSet> plans;
+  uint64_t plans_generation = ~0ull;
   explicit hawk_engine(int d) : engine(d) {}
 };
 
 struct hawk_result {
-  Table table{"result", {}};
+  ResultColumns table;
   ExecutionMetrics metrics;
   std::string metrics_text;
 };
@@ -72,6 +76,20 @@ PipelineSet plan_sql(Engine& engine, const std::string& sql) {
   const std::vector<TablePtr> tables = engine.catalog();
   auto plan = sql::parse_query(sql, sql::make_catalog(tables));
   return partition_into_pipelines(plan, tables);
+}
+
+// plan_sql with the engine's plan cache (parse + partition once per catalog state)
+const PipelineSet& cached_plan(hawk_engine* e, const std::string& sql) {
+  if (e->plans_generation != e->engine.catalog_generation()) {
+    e->plans.clear();
+    e->plans_generation = e->engine.catalog_generation();
+  }
+  auto it = e->plans.find(sql);
+  if (it == e->plans.end()) {
+    if (e->plans.size() > 256) e->plans.clear();
+    it = e->plans.emplace(sql, plan_sql(e->engine, sql)).first;
+  }
+  return it->second;
 }
 
 // "<proj>;<agg>" workload config, or "c0|c1|..." one per pipeline
@@ -169,11 +187,11 @@ int32_t hawk_engine_flush_l2(hawk_engine* e) {
 int32_t hawk_engine_run(hawk_engine* e, const char* sql, const char* config, hawk_result** out) {
   *out = nullptr;
   return guard([&] {
-    PipelineSet set = plan_sql(e->engine, sql);
+    const PipelineSet& set = cached_plan(e, sql);
     auto configs = configs_for(set, config ? config : "");
     auto* r = new hawk_result;
     try {
-      r->table = e->engine.execute(set, configs, &r->metrics);
+      r->table = e->engine.execute_columns(set, configs, &r->metrics);
     } catch (...) {
       delete r;
       throw;
@@ -187,7 +205,7 @@ int32_t hawk_engine_run_partial(hawk_engine* e, const char* sql, const char* con
                                 hawk_partial** out) {
   *out = nullptr;
   return guard([&] {
-    PipelineSet set = plan_sql(e->engine, sql);
+    const PipelineSet& set = cached_plan(e, sql);
     WorkloadConfig w = config && *config ? parse_workload_config(config) : WorkloadConfig();
     auto* p = new hawk_partial;
     ExecutionMetrics m;
@@ -215,7 +233,7 @@ int32_t hawk_engine_finalize(hawk_engine* e, const char* sql, const char* config
                              const int64_t* const* data, const int64_t* rows, hawk_result** out) {
   *out = nullptr;
   return guard([&] {
-    PipelineSet set = plan_sql(e->engine, sql);
+    const PipelineSet& set = cached_plan(e, sql);
     WorkloadConfig w = config && *config ? parse_workload_config(config) : WorkloadConfig();
     // widths come from the lowered terminal program
     const std::size_t T = static_cast<std::size_t>(set.terminal);
@@ -236,7 +254,7 @@ int32_t hawk_engine_finalize(hawk_engine* e, const char* sql, const char* config
     }
     auto* r = new hawk_result;
     try {
-      r->table = e->engine.finalize_partials(set, w, parts);
+      r->table = e->engine.finalize_partials_columns(set, w, parts);
     } catch (...) {
       delete r;
       throw;
@@ -245,24 +263,24 @@ int32_t hawk_engine_finalize(hawk_engine* e, const char* sql, const char* config
   });
 }
 
-int64_t hawk_result_rows(const hawk_result* r) { return static_cast<int64_t>(r->table.row_count()); }
-int32_t hawk_result_ncols(const hawk_result* r) { return static_cast<int32_t>(r->table.column_count()); }
+int64_t hawk_result_rows(const hawk_result* r) { return r->table.rows; }
+int32_t hawk_result_ncols(const hawk_result* r) { return static_cast<int32_t>(r->table.columns.size()); }
 const char* hawk_result_col_name(const hawk_result* r, int32_t c) {
-  return r->table.column_name(static_cast<std::size_t>(c)).c_str();
+  return r->table.columns[static_cast<std::size_t>(c)].name.c_str();
 }
 int32_t hawk_result_col_kind(const hawk_result* r, int32_t c) {
-  return static_cast<int32_t>(r->table.column(static_cast<std::size_t>(c)).kind());
+  return static_cast<int32_t>(r->table.columns[static_cast<std::size_t>(c)].kind);
 }
 const void* hawk_result_col_data(const hawk_result* r, int32_t c) {
-  const Column& col = r->table.column(static_cast<std::size_t>(c));
-  if (col.kind() == ColumnKind::Float64) return col.floats().data();
-  return col.ints().data();
+  const ResultColumn& col = r->table.columns[static_cast<std::size_t>(c)];
+  if (col.kind == ColumnKind::Float64) return col.floats.data();
+  return col.ints.data();
 }
 int64_t hawk_result_col_lexicon_size(const hawk_result* r, int32_t c) {
-  return static_cast<int64_t>(r->table.column(static_cast<std::size_t>(c)).lexicon().size());
+  return static_cast<int64_t>(r->table.columns[static_cast<std::size_t>(c)].lexicon.size());
 }
 const char* hawk_result_col_lexicon(const hawk_result* r, int32_t c, int64_t i) {
-  return r->table.column(static_cast<std::size_t>(c)).lexicon()[static_cast<std::size_t>(i)].c_str();
+  return r->table.columns[static_cast<std::size_t>(c)].lexicon[static_cast<std::size_t>(i)].c_str();
 }
 double hawk_result_kernel_ms(const hawk_result* r) { return r->metrics.kernel_ms; }
 double hawk_result_wall_ms(const hawk_result* r) { return r->metrics.wall_ms; }

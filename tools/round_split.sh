@@ -1,0 +1,20 @@
+fmt='import sys, json
+for l in sys.stdin:
+    try: d = json.loads(l)
+    except Exception: print(l.strip()[:300]); continue
+    print(d["query"], round(d.get("kernel_ms", -1), 4), d["config"][:110], d.get("error", "")[:200], [round(p["kernel_ms"],3) for p in d.get("pipelines", [])])'
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+P="single_pass/coalesced/branched"
+for c in 1 0; do
+for q in ssb_q41 tpch_q3 ssb_q11; do
+echo "== $q compact=$c"
+timeout 600 python bench.py --query $q --compact $c --sweep \
+ "$P;global_hash/coalesced/branched/linear_probing/multiply_shift/wg=256" \
+ "$P;global_hash/coalesced/branched/cuckoo/multiply_shift/wg=256" \
+ "$P;global_hash/coalesced/branched/linear_probing/murmur/wg=256" \
+ "$P;local_hash/coalesced/branched/linear_probing/multiply_shift/wg=256/ht=8" \
+ "$P/u=2;global_hash/coalesced/branched/linear_probing/multiply_shift/wg=256/u=2" \
+ "$P;global_hash/sequential/branched/linear_probing/multiply_shift/wg=256" \
+ 2>&1 | python3 -c "$fmt"
+done
+done
