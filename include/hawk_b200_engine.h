@@ -109,6 +109,14 @@ int32_t hawk_engine_learn(hawk_engine* e, const char* const* sqls, int32_t n, in
                           double prune_ms, int32_t reps, char* best, int32_t len, double* best_ms,
                           int32_t* evaluations, int32_t* sweeps);
 
+/* Algorithm 1 over a caller-supplied cost: cost(config)
+ * returns the time of a workload configuration in to_string() format
+ * (INFINITY = failed/pruned). No engine or GPU involved. */
+typedef double (*hawk_cost_fn)(const char* config, void* user);
+int32_t hawk_learn_with_cost(hawk_cost_fn cost, void* user, int32_t q, int32_t early_termination,
+                             char* best, int32_t len, double* best_ms, int32_t* evaluations,
+                             int32_t* sweeps);
+
 #ifdef __cplusplus
 }
 #endif

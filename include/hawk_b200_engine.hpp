@@ -269,6 +269,10 @@ struct LearnResult {
 /// by configuration key, strict-< keeps the earlier value.
 LearnResult learn_variant_configuration(Engine& engine, const std::vector<WorkloadQuery>& workload,
                                         const LearnOptions& opt);
+/// Algorithm 1 over any cost function (the learner above with `cost` =
+/// measure_variant); used directly by the CPU tests with synthetic costs.
+LearnResult coordinate_descent(const std::vector<Dimension>& dims, const LearnOptions& opt,
+                               const std::function<Measurement(const WorkloadConfig&)>& cost);
 /// Brute force over explicit configurations.
 LearnResult full_exploration(Engine& engine, const std::vector<WorkloadQuery>& workload,
                              const std::vector<WorkloadConfig>& space, const LearnOptions& opt);

@@ -426,4 +426,24 @@ int32_t hawk_engine_learn(hawk_engine* e, const char* const* sqls, int32_t n, in
   });
 }
 
+int32_t hawk_learn_with_cost(hawk_cost_fn cost, void* user, int32_t q, int32_t early_termination,
+                             char* best, int32_t len, double* best_ms, int32_t* evaluations,
+                             int32_t* sweeps) {
+  return guard([&] {
+    if (!cost) throw InvalidParams("no cost function");
+    LearnOptions opt;
+    opt.max_iterations = q;
+    opt.early_termination = early_termination != 0;
+    LearnResult r = coordinate_descent(workload_dimensions(), opt, [&](const WorkloadConfig& c) {
+      Measurement m;
+      m.ms = cost(c.to_string().c_str(), user);
+      return m;
+    });
+    put_str(best, len, r.best.to_string());
+    *best_ms = r.best_ms;
+    *evaluations = r.evaluations;
+    *sweeps = r.sweeps;
+  });
+}
+
 }  // extern "C"

@@ -3,6 +3,7 @@
 // on the device the way the paper times every variant on its processor.
 #include <algorithm>
 #include <cmath>
+#include <functional>
 #include <map>
 
 #include "hawk/sql/parser.hpp"
@@ -27,6 +28,13 @@ std::vector<PreparedQuery> prepare(Engine& engine, const std::vector<WorkloadQue
   return out;
 }
 
+std::vector<VariantConfiguration> per_kind(const PipelineSet& set, const WorkloadConfig& c) {
+  std::vector<VariantConfiguration> v;
+  for (const PipelineProgram& p : set.pipelines)
+    v.push_back(p.kind == PipelineKind::Projection ? c.projection : c.aggregation);
+  return v;
+}
+
 Measurement measure(Engine& engine, const WorkloadConfig& config,
                     const std::vector<PreparedQuery>& queries, const LearnOptions& opt) {
   Measurement m;
@@ -37,7 +45,8 @@ Measurement measure(Engine& engine, const WorkloadConfig& config,
     try {
       for (int r = 0; r < std::max(1, opt.repetitions); ++r) {
         ExecutionMetrics em;
-        engine.execute(q.set, config, &em);
+        engine.flush_l2();  // every run starts from HBM, as the paper's cold runs
+        engine.execute_columns(q.set, per_kind(q.set, config), &em);
         times.push_back(em.kernel_ms);
         // slow variants are pruned after one run
         if (em.kernel_ms > opt.prune_threshold_ms) break;
@@ -68,10 +77,8 @@ Measurement measure_variant(Engine& engine, const WorkloadConfig& config,
   return measure(engine, config, prepare(engine, workload), opt);
 }
 
-LearnResult learn_variant_configuration(Engine& engine, const std::vector<WorkloadQuery>& workload,
-                                        const LearnOptions& opt) {
-  const std::vector<PreparedQuery> queries = prepare(engine, workload);
-  const std::vector<Dimension> dims = workload_dimensions();
+LearnResult coordinate_descent(const std::vector<Dimension>& dims, const LearnOptions& opt,
+                               const std::function<Measurement(const WorkloadConfig&)>& cost) {
   LearnResult res;
   // base configuration: the first value of every dimension (Algorithm 1 line 1)
   std::vector<int> cur(dims.size(), 0);
@@ -86,7 +93,8 @@ LearnResult learn_variant_configuration(Engine& engine, const std::vector<Worklo
     const std::string key = c.to_string();
     auto it = cache.find(key);
     if (it != cache.end()) return it->second.ms;
-    Measurement m = measure(engine, c, queries, opt);
+    Measurement m = cost(c);
+    m.config = c;
     ++res.evaluations;
     res.trace.push_back(m);
     cache[key] = m;
@@ -112,12 +120,19 @@ LearnResult learn_variant_configuration(Engine& engine, const std::vector<Worklo
       }
     }
     ++res.sweeps;
-    if (!changed) break;  // Algorithm 1 lines 19-21
-    if (opt.early_termination && sweep + 1 >= opt.max_iterations) break;
+    if (opt.early_termination && !changed) break;  // Algorithm 1 lines 19-21
   }
   res.best = config_of(cur);
   res.best_ms = eval(cur);
   return res;
+}
+
+LearnResult learn_variant_configuration(Engine& engine, const std::vector<WorkloadQuery>& workload,
+                                        const LearnOptions& opt) {
+  const std::vector<PreparedQuery> queries = prepare(engine, workload);
+  return coordinate_descent(workload_dimensions(), opt, [&](const WorkloadConfig& c) {
+    return measure(engine, c, queries, opt);
+  });
 }
 
 LearnResult full_exploration(Engine& engine, const std::vector<WorkloadQuery>& workload,

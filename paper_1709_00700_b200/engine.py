@@ -141,16 +141,37 @@ class Result:
         raise KeyError(name)
 
 
+class _ResultOwner:
+    """Frees a hawk_result once no column array views its memory any more."""
+
+    def __init__(self, lib, r):
+        self.lib, self.r = lib, r
+
+    def __del__(self):
+        try:
+            self.lib.hawk_result_free(self.r)
+        except Exception:
+            pass
+
+
 def _result_from(lib, r) -> Result:
+    """Result columns are zero-copy views of the engine's result buffers; the
+    hawk_result lives as long as any of them (large results, e.g. TPC-H Q3
+    SF100's 1.2M groups, are not copied again)."""
     cols = []
+    owner = _ResultOwner(lib, r)
     n = lib.hawk_result_rows(r)
     for c in range(lib.hawk_result_ncols(r)):
         kind = lib.hawk_result_col_kind(r, c)
         name = lib.hawk_result_col_name(r, c).decode()
         ptr = lib.hawk_result_col_data(r, c)
         dtype = np.float64 if kind == FLOAT64 else np.int64
-        vals = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_double if kind == FLOAT64 else C.c_int64)),
-                                     shape=(n,)).copy() if n else np.zeros(0, dtype)
+        if n:
+            buf = ((C.c_double if kind == FLOAT64 else C.c_int64) * n).from_address(ptr)
+            buf._owner = owner
+            vals = np.ctypeslib.as_array(buf)
+        else:
+            vals = np.zeros(0, dtype)
         lex = None
         if kind == STRING:
             lex = [lib.hawk_result_col_lexicon(r, c, i).decode()
@@ -249,10 +270,7 @@ class Engine:
     def run(self, sql: str, config: str = "") -> Result:
         r = C.c_void_p()
         _check(self._lib.hawk_engine_run(self._h, sql.encode(), config.encode(), C.byref(r)))
-        try:
-            return _result_from(self._lib, r)
-        finally:
-            self._lib.hawk_result_free(r)
+        return _result_from(self._lib, r)  # frees r when the columns are gone
 
     def run_partial(self, sql: str, config: str = "") -> "Partial":
         """Shard execution: the (rows x width) int64 partials before the cross-GPU merge."""
@@ -277,10 +295,7 @@ class Engine:
         r = C.c_void_p()
         _check(self._lib.hawk_engine_finalize(self._h, sql.encode(), config.encode(), len(arrs),
                                               data, rows, C.byref(r)))
-        try:
-            return _result_from(self._lib, r)
-        finally:
-            self._lib.hawk_result_free(r)
+        return _result_from(self._lib, r)  # frees r when the columns are gone
 
     # ---- IR introspection ----
     def pipeline_count(self, sql: str) -> int:

@@ -1,0 +1,75 @@
+"""Algorithm 1 on CPU: the engine's
+coordinate descent (engine/learner.cpp) driven through the C ABI with
+synthetic costs instead of CUDA-event measurements."""
+import ctypes as C
+import math
+
+from paper_1709_00700_b200 import _native
+
+# preferred value per workload dimension (SPEC.md:244-252 value lists)
+PREFER = {
+    "proj": "multi_pass", "agg": "local_hash", "tm": "tm=1024", "wg": "wg=64",
+    "access": "coalesced", "ht": "ht=64", "pred": "predicated", "impl": "cuckoo",
+    "fn": "multiply_shift",
+}
+
+
+def fields(config: str) -> dict:
+    proj, agg = config.split(";")
+    p, a = proj.split("/"), agg.split("/")
+    f = {"proj": p[0], "agg": a[0], "access": a[1], "pred": a[2], "impl": a[3], "fn": a[4]}
+    for part in p + a:
+        for key in ("tm", "wg", "ht"):
+            if part.startswith(key + "="):
+                f[key] = part
+    return f
+
+
+def learn(cost, q=3, early=1):
+    lib = _native.engine()
+    calls = []
+
+    def cb(cfg, _user):
+        calls.append(cfg.decode())
+        return cost(cfg.decode())
+
+    fn = _native.COST_FN(cb)
+    best = C.create_string_buffer(512)
+    ms, ev, sw = C.c_double(), C.c_int32(), C.c_int32()
+    assert lib.hawk_learn_with_cost(fn, None, q, early, best, 512, C.byref(ms), C.byref(ev),
+                                    C.byref(sw)) == 0, lib.hawk_engine_last_error()
+    return best.value.decode(), ms.value, ev.value, sw.value, calls
+
+
+def separable(cfg: str) -> float:
+    f = fields(cfg)
+    return 1.0 + sum(0.0 if f.get(k) == v else 1.0 for k, v in PREFER.items())
+
+
+def test_separable_cost_reaches_optimum_in_one_sweep():
+    best, ms, ev, sw, calls = learn(separable)
+    f = fields(best)
+    for k, v in PREFER.items():
+        assert f.get(k) == v, (k, best)
+    assert ms == 1.0
+    assert sw == 2  # the second sweep changes nothing: early termination
+    assert ev == len(calls) == len(set(calls))  # every configuration measured once (cache)
+
+
+def test_ties_keep_the_current_value_and_q_bounds_sweeps():
+    # flat cost: nothing ever beats the base configuration (strict <)
+    best, ms, ev, sw, _ = learn(lambda cfg: 5.0, q=3)
+    base, *_ = learn(lambda cfg: 5.0, q=1)
+    assert best == base and ms == 5.0 and sw == 1
+    # without early termination all q sweeps run
+    *_, sw3, _ = learn(separable, q=3, early=0)
+    assert sw3 == 3
+
+
+def test_failed_variants_are_infinite():
+    # variants that "fail" (inf) are never chosen
+    def cost(cfg):
+        f = fields(cfg)
+        return math.inf if f["impl"] == "cuckoo" else separable(cfg)
+    best, ms, *_ = learn(cost)
+    assert fields(best)["impl"] == "linear_probing" and math.isfinite(ms)
