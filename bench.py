@@ -31,7 +31,7 @@ DEFAULT_CONFIG = {
     "tpch_q1": "single_pass/coalesced/branched;local_hash/coalesced/predicated/linear_probing/murmur/wg=256/ht=8",
     "ssb_q11": "single_pass/coalesced/branched;global_hash/coalesced/branched/linear_probing/multiply_shift/wg=256",
     "ssb_q41": "single_pass/coalesced/branched;global_hash/coalesced/branched/linear_probing/multiply_shift/wg=256",
-    "tpch_q3": "single_pass/coalesced/branched/u=2;global_hash/coalesced/branched/linear_probing/multiply_shift/wg=256",
+    "tpch_q3": "single_pass/coalesced/branched/u=4;global_hash/coalesced/branched/linear_probing/multiply_shift/wg=64",
 }
 DEFAULT_SF = {"tpch_q6": 1.0, "tpch_q1": 10.0, "ssb_q11": 10.0, "ssb_q41": 10.0, "tpch_q3": 10.0}
 WORKLOAD_NAME = {"tpch_q6": "TPC-H Q6", "tpch_q1": "TPC-H Q1", "ssb_q11": "SSB Q1.1",
@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--cpu-sample-rows", type=int, default=4_000_000)
     ap.add_argument("--prefetch", type=int, default=None, help="TMA pipeline depth (pass tiles)")
     ap.add_argument("--stage", type=int, default=1, help="1: TMA-staged pass tiles (coalesced)")
+    ap.add_argument("--min-ctas", type=int, default=None,
+                    help="compiled programs: __launch_bounds__ minimum CTAs per SM")
     ap.add_argument("--compact", type=int, default=None,
                     help="compiled, branched: compact live rows after the first probe (1) or not (0)")
     ap.add_argument("--pass-sync", type=int, default=None,
@@ -105,6 +107,8 @@ def run_sweep(args):
         engine.set_option("pass_sync", args.pass_sync)
     if args.compact is not None:
         engine.set_option("compact", args.compact)
+    if args.min_ctas is not None:
+        engine.set_option("min_ctas", args.min_ctas)
     load_tables(engine, query, sf, args.seed, 0, 1)
     sql = Q.BENCH[query][0]
     for cfg in (args.sweep or SWEEP):
@@ -339,6 +343,8 @@ def main():
         engine.set_option("pass_sync", args.pass_sync)
     if args.compact is not None:
         engine.set_option("compact", args.compact)
+    if args.min_ctas is not None:
+        engine.set_option("min_ctas", args.min_ctas)
     per_rank = load_tables(engine, query, sf, args.seed, rank, world)
     lib = _native.b200()
     stream = torch.cuda.ExternalStream(lib.hawk_b200_ctx_stream(engine.ctx), device=torch.device("cuda", local))

@@ -260,6 +260,7 @@ int32_t hawk_b200_ctx_synchronize(hawk_ctx* ctx);
  * "stage_probes" (pipelines with probes staged/synchronised too; default 0),
  * "dense_keys" (HASH_AGGREGATE: use hawk_pipeline.dense_groups; default 1),
  * "compact" (compiled, branched: compact live rows after the first probe; default 1),
+ * "min_ctas" (compiled: __launch_bounds__ minimum CTAs per SM; 0 = by unroll),
  * "priv_groups" (HASH_AGGREGATE local: groups with thread-private accumulators). */
 int32_t hawk_b200_ctx_set_option(hawk_ctx* ctx, const char* name, int64_t value);
 

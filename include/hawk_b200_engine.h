@@ -114,8 +114,10 @@ int32_t hawk_engine_learn(hawk_engine* e, const char* const* sqls, int32_t n, in
  * (INFINITY = failed/pruned). No engine or GPU involved. */
 typedef double (*hawk_cost_fn)(const char* config, void* user);
 int32_t hawk_learn_with_cost(hawk_cost_fn cost, void* user, int32_t q, int32_t early_termination,
-                             char* best, int32_t len, double* best_ms, int32_t* evaluations,
-                             int32_t* sweeps);
+                             const char* starts, char* best, int32_t len, double* best_ms,
+                             int32_t* evaluations, int32_t* sweeps);
+/* starts: NULL = the reference default configuration; else '|'-separated
+ * workload configurations, one descent from each (shared cache, best kept) */
 
 #ifdef __cplusplus
 }

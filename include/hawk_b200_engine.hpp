@@ -236,6 +236,13 @@ struct LearnOptions {
   bool early_termination = true;     // stop at the first unchanged sweep
   double prune_threshold_ms = 1000;  // slow-variant pruning
   int repetitions = 3;               // timed runs per query (median)
+  /// Starting configurations of the descent (Algorithm 1 line 1). Empty =
+  /// the reference's default VariantConfiguration (every dimension's first
+  /// value); more than one = restarts sharing one measurement cache, best
+  /// result kept. Coordinate descent from the reference default can stall in
+  /// a pruned region (e.g. TPC-H Q1: local_hash with wg=16/ht=1 is pruned, so
+  /// global_hash wins dimension 2 and is never left).
+  std::vector<WorkloadConfig> starts;
 };
 
 struct Measurement {
@@ -273,6 +280,9 @@ LearnResult learn_variant_configuration(Engine& engine, const std::vector<Worklo
 /// measure_variant); used directly by the CPU tests with synthetic costs.
 LearnResult coordinate_descent(const std::vector<Dimension>& dims, const LearnOptions& opt,
                                const std::function<Measurement(const WorkloadConfig&)>& cost);
+/// The B200 starting point used as the learner's second start: single-pass
+/// coalesced branched projections; local_hash, wg=256, ht=8, linear probing.
+WorkloadConfig b200_start_config();
 /// Brute force over explicit configurations.
 LearnResult full_exploration(Engine& engine, const std::vector<WorkloadQuery>& workload,
                              const std::vector<WorkloadConfig>& space, const LearnOptions& opt);

@@ -139,7 +139,7 @@ def engine() -> C.CDLL:
              C.POINTER(f64))
         _sig(lib, "hawk_engine_learn", i32, vp, C.POINTER(cp), i32, i32, f64, i32, cp, i32,
              C.POINTER(f64), C.POINTER(i32), C.POINTER(i32))
-        _sig(lib, "hawk_learn_with_cost", i32, COST_FN, vp, i32, i32, cp, i32, C.POINTER(f64),
+        _sig(lib, "hawk_learn_with_cost", i32, COST_FN, vp, i32, i32, cp, cp, i32, C.POINTER(f64),
              C.POINTER(i32), C.POINTER(i32))
         _engine = lib
     return _engine

@@ -29,6 +29,7 @@ struct hawk_ctx {
   int stage_probes = 0;     // COALESCED pipelines with probes: TMA staging + barrier too
   int dense_keys = 1;       // HAGG_LOCAL compiled: dense key-index lookaside when provided
   int compact = 1;          // compiled, branched: compact live rows after the first probe
+  int min_ctas = 0;         // compiled: __launch_bounds__ min CTAs/SM override (0 = default)
   int priv_groups = 64;     // HAGG_LOCAL: groups with thread-private accumulators
   int jit = 0;              // compiled programs (jit.cu) instead of the interpreter
   int stage = 1;            // COALESCED: stage pass tiles in smem with TMA
@@ -332,6 +333,7 @@ int32_t prepare(hawk_ctx* ctx, const hawk_pipeline& pipe, const hawk_variant& v,
   // live-row compaction after the first probe (compiled, branched; the
   // multi-pass roles need CTA-uniform control flow and keep the R-row path)
   kp.split = ctx->jit && ctx->compact && split_rows_for(pipe, v, role);
+  kp.min_ctas = ctx->min_ctas;
   shape.jit_fn = nullptr;
   if (ctx->jit) {  // compiled program: generate + NVRTC (cached), see jit.cu
     std::string err;
@@ -514,6 +516,10 @@ int32_t hawk_b200_ctx_set_option(hawk_ctx* ctx, const char* name, int64_t value)
   }
   if (std::strcmp(name, "l2_distance") == 0) {
     ctx->l2_distance = (int)std::max<int64_t>(0, std::min<int64_t>(value, 16));
+    return HAWK_OK;
+  }
+  if (std::strcmp(name, "min_ctas") == 0) {
+    ctx->min_ctas = (int)std::max<int64_t>(0, std::min<int64_t>(value, 8));
     return HAWK_OK;
   }
   if (std::strcmp(name, "compact") == 0) {

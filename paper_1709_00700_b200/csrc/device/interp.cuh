@@ -88,6 +88,7 @@ struct KParams {
   int32_t smem_priv_off;              // HAGG_LOCAL: priv[(ord * naggs + a) * B + t]
   int32_t smem_dense_off;             // HAGG_LOCAL, compiled: dense key index -> ordinal (0: off)
   int32_t split;                      // compiled, branched: compact live rows after the first probe
+  int32_t min_ctas;                   // compiled: __launch_bounds__ min CTAs per SM (0 = by unroll)
   int32_t smem_queue_off;             //   ... per-warp queues of (row, probe-0 row id)
   int32_t smem_state_off;
   int32_t state_words;                // state words per thread

@@ -418,6 +418,8 @@ int32_t hawk_engine_learn(hawk_engine* e, const char* const* sqls, int32_t n, in
     opt.max_iterations = q;
     opt.prune_threshold_ms = prune_ms;
     opt.repetitions = reps;
+    // Algorithm 1 from the reference default, then from the B200 start
+    opt.starts = {WorkloadConfig(), b200_start_config()};
     LearnResult r = learn_variant_configuration(e->engine, w, opt);
     put_str(best, len, r.best.to_string());
     *best_ms = r.best_ms;
@@ -427,13 +429,18 @@ int32_t hawk_engine_learn(hawk_engine* e, const char* const* sqls, int32_t n, in
 }
 
 int32_t hawk_learn_with_cost(hawk_cost_fn cost, void* user, int32_t q, int32_t early_termination,
-                             char* best, int32_t len, double* best_ms, int32_t* evaluations,
-                             int32_t* sweeps) {
+                             const char* starts, char* best, int32_t len, double* best_ms,
+                             int32_t* evaluations, int32_t* sweeps) {
   return guard([&] {
     if (!cost) throw InvalidParams("no cost function");
     LearnOptions opt;
     opt.max_iterations = q;
     opt.early_termination = early_termination != 0;
+    if (starts && *starts) {
+      std::stringstream ss(starts);
+      std::string part;
+      while (std::getline(ss, part, '|')) opt.starts.push_back(parse_workload_config(part));
+    }
     LearnResult r = coordinate_descent(workload_dimensions(), opt, [&](const WorkloadConfig& c) {
       Measurement m;
       m.ms = cost(c.to_string().c_str(), user);

@@ -77,15 +77,33 @@ Measurement measure_variant(Engine& engine, const WorkloadConfig& config,
   return measure(engine, config, prepare(engine, workload), opt);
 }
 
+WorkloadConfig b200_start_config() {
+  return parse_workload_config(
+      "single_pass/coalesced/branched;local_hash/coalesced/branched/linear_probing/murmur/wg=256/ht=8");
+}
+
 LearnResult coordinate_descent(const std::vector<Dimension>& dims, const LearnOptions& opt,
                                const std::function<Measurement(const WorkloadConfig&)>& cost) {
   LearnResult res;
-  // base configuration: the first value of every dimension (Algorithm 1 line 1)
-  std::vector<int> cur(dims.size(), 0);
   auto config_of = [&](const std::vector<int>& idx) {
     WorkloadConfig c;
     for (std::size_t d = 0; d < dims.size(); ++d) dims[d].set(c, idx[d]);
     return c;
+  };
+  // dimension value indices of a configuration (values not on a dimension's
+  // list fall back to its first value)
+  auto index_of = [&](const WorkloadConfig& c) {
+    std::vector<int> idx(dims.size(), 0);
+    for (std::size_t d = 0; d < dims.size(); ++d)
+      for (int v = 0; v < static_cast<int>(dims[d].values.size()); ++v) {
+        WorkloadConfig t = c;
+        dims[d].set(t, v);
+        if (t.to_string() == c.to_string()) {
+          idx[d] = v;
+          break;
+        }
+      }
+    return idx;
   };
   std::map<std::string, Measurement> cache;  // measurements by configuration key
   auto eval = [&](const std::vector<int>& idx) -> double {
@@ -100,30 +118,42 @@ LearnResult coordinate_descent(const std::vector<Dimension>& dims, const LearnOp
     cache[key] = m;
     return m.ms;
   };
-  for (int sweep = 0; sweep < opt.max_iterations; ++sweep) {
-    bool changed = false;
-    for (std::size_t d = 0; d < dims.size(); ++d) {   // feature order
-      int best_v = cur[d];
-      double best = eval(cur);
-      for (int v = 0; v < static_cast<int>(dims[d].values.size()); ++v) {
-        std::vector<int> cand = cur;
-        cand[d] = v;
-        const double ms = eval(cand);
-        if (ms < best) {  // strict <: ties keep the earlier value
-          best = ms;
-          best_v = v;
+  std::vector<std::vector<int>> starts;
+  if (opt.starts.empty()) starts.emplace_back(dims.size(), 0);  // Algorithm 1 line 1
+  for (const WorkloadConfig& c : opt.starts) starts.push_back(index_of(c));
+  bool first = true;
+  for (std::vector<int> cur : starts) {
+    int sweeps = 0;
+    for (int sweep = 0; sweep < opt.max_iterations; ++sweep) {
+      bool changed = false;
+      for (std::size_t d = 0; d < dims.size(); ++d) {   // feature order
+        int best_v = cur[d];
+        double best = eval(cur);
+        for (int v = 0; v < static_cast<int>(dims[d].values.size()); ++v) {
+          std::vector<int> cand = cur;
+          cand[d] = v;
+          const double ms = eval(cand);
+          if (ms < best) {  // strict <: ties keep the earlier value
+            best = ms;
+            best_v = v;
+          }
+        }
+        if (best_v != cur[d]) {
+          cur[d] = best_v;
+          changed = true;
         }
       }
-      if (best_v != cur[d]) {
-        cur[d] = best_v;
-        changed = true;
-      }
+      ++sweeps;
+      if (opt.early_termination && !changed) break;  // Algorithm 1 lines 19-21
     }
-    ++res.sweeps;
-    if (opt.early_termination && !changed) break;  // Algorithm 1 lines 19-21
+    const double ms = eval(cur);
+    if (first || ms < res.best_ms) {
+      res.best = config_of(cur);
+      res.best_ms = ms;
+      res.sweeps = sweeps;
+    }
+    first = false;
   }
-  res.best = config_of(cur);
-  res.best_ms = eval(cur);
   return res;
 }
 

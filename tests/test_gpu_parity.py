@@ -316,3 +316,27 @@ def test_sf1_matches_port(engine):
                     assert abs(x - y) <= 1e-9 * max(1.0, abs(x), abs(y)), (key, a, b)
     for t in ("lineitem", "orders", "customer"):
         engine.drop(t)
+
+
+@pytest.mark.parametrize("key", sorted(Q.BENCH))
+def test_sf10_bench_queries_match_port(key):
+    """The BASELINE workloads at SF10 (bench sizes) under the bench's default
+    variants, against the pinned multi-threaded CPU restatement."""
+    import bench
+    from test_oracle import port_rows
+    sql, tables, fact = Q.BENCH[key]
+    e = Engine(0)
+    try:
+        e.set_option("jit", 1)
+        for t in tables:
+            e.generate(t, 10.0, 42)
+        expected = port_rows(key, 10.0, 42, threads=os.cpu_count() or 8)
+        for cfg in (bench.DEFAULT_CONFIG[key], CONFIGS[1]):
+            got = e.run(sql, cfg)
+            rows = sorted(zip(*[c.values.tolist() for c in got.columns]))
+            assert len(rows) == len(expected), (key, cfg)
+            for a, b in zip(rows, expected):
+                for x, y in zip(a, b):
+                    assert abs(x - y) <= 1e-9 * max(1.0, abs(x), abs(y)), (key, cfg, a, b)
+    finally:
+        e.close()

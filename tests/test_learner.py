@@ -25,7 +25,7 @@ def fields(config: str) -> dict:
     return f
 
 
-def learn(cost, q=3, early=1):
+def learn(cost, q=3, early=1, starts=None):
     lib = _native.engine()
     calls = []
 
@@ -36,8 +36,9 @@ def learn(cost, q=3, early=1):
     fn = _native.COST_FN(cb)
     best = C.create_string_buffer(512)
     ms, ev, sw = C.c_double(), C.c_int32(), C.c_int32()
-    assert lib.hawk_learn_with_cost(fn, None, q, early, best, 512, C.byref(ms), C.byref(ev),
-                                    C.byref(sw)) == 0, lib.hawk_engine_last_error()
+    assert lib.hawk_learn_with_cost(fn, None, q, early, starts.encode() if starts else None, best,
+                                    512, C.byref(ms), C.byref(ev), C.byref(sw)) == 0, \
+        lib.hawk_engine_last_error()
     return best.value.decode(), ms.value, ev.value, sw.value, calls
 
 
@@ -73,3 +74,27 @@ def test_failed_variants_are_infinite():
         return math.inf if f["impl"] == "cuckoo" else separable(cfg)
     best, ms, *_ = learn(cost)
     assert fields(best)["impl"] == "linear_probing" and math.isfinite(ms)
+
+
+B200_START = "single_pass/coalesced/branched;local_hash/coalesced/branched/linear_probing/murmur/wg=256/ht=8"
+
+
+def trap(cfg: str) -> float:
+    """TPC-H Q1-like landscape: local_hash is pruned (inf) at small work
+    groups, global_hash is slow everywhere, local_hash with wg >= 128 is fast."""
+    f = fields(cfg)
+    if f["agg"] == "global_hash":
+        return 100.0
+    wg = int(f["wg"].split("=")[1])
+    return math.inf if wg < 128 else 1.0 + (0.0 if f.get("ht") == "ht=8" else 0.5)
+
+
+def test_restart_escapes_a_pruned_region():
+    # from the reference default (wg=16) the descent settles on global_hash ...
+    best, ms, *_ = learn(trap)
+    assert fields(best)["agg"] == "global_hash" and ms == 100.0
+    # ... a second start in the fast region (shared cache) finds local_hash
+    best2, ms2, *_ = learn(trap, starts="|".join([
+        "single_pass/sequential/branched;local_hash/sequential/branched/linear_probing/murmur/wg=16/ht=1",
+        B200_START]))
+    assert fields(best2)["agg"] == "local_hash" and ms2 == 1.0
