@@ -29,7 +29,7 @@ METRIC = "input tuples/sec & HBM GB/s (roofline frac) per TPC-H/SSB query, 1/2/4
 DEFAULT_CONFIG = {
     "tpch_q6": "single_pass/sequential/branched/u=2;global_hash/sequential/branched/linear_probing/multiply_shift/wg=256/u=2",
     "tpch_q1": "single_pass/coalesced/branched;local_hash/coalesced/predicated/linear_probing/murmur/wg=256/ht=8",
-    "ssb_q11": "single_pass/coalesced/branched;global_hash/coalesced/branched/linear_probing/multiply_shift/wg=256",
+    "ssb_q11": "single_pass/coalesced/branched/u=4;global_hash/coalesced/branched/linear_probing/multiply_shift/wg=64",
     "ssb_q41": "single_pass/coalesced/branched;global_hash/coalesced/branched/linear_probing/multiply_shift/wg=256",
     "tpch_q3": "single_pass/coalesced/branched/u=4;global_hash/coalesced/branched/linear_probing/multiply_shift/wg=64",
 }

@@ -135,8 +135,8 @@ typedef struct hawk_arith {
 
 /* HASH_PROBE (ir/program.hpp:113-116): looks `key` up in table `table` */
 typedef struct hawk_probe {
-  int32_t table; /* index into hawk_pipeline.tables */
-  int32_t pad;
+  int32_t table;       /* index into hawk_pipeline.tables */
+  int32_t filter_only; /* 1: no operand reads this probe's build payload (semi-join) */
   hawk_operand key;
 } hawk_probe;
 
@@ -162,7 +162,15 @@ typedef struct hawk_table {
   int32_t log2_capacity;
   int32_t key_arity;
   int32_t slot_words; /* 2 for join tables */
-  int32_t pad;
+  int32_t bits_copies; /* replicas of d_bits (small bitmaps are replicated so
+                        * every SM does not hammer the same few L2 lines) */
+  /* join tables with a small key range: bit (key - bits_lo) of d_bits is set
+   * for every inserted key (exact membership; NULL = none). Probes whose build
+   * payload is never read test the bit instead of walking the table. Replica
+   * c occupies words [c * W, (c + 1) * W) with W = ceil(bits_span / 64). */
+  uint64_t* d_bits;
+  int64_t bits_lo;
+  int64_t bits_span;
 } hawk_table;
 
 /* A lowered pipeline program: LOOP over the driver, FILTER conjuncts on the

@@ -63,6 +63,24 @@ __device__ __forceinline__ u64 as_bits(double d) { return (u64)__double_as_longl
 __device__ __forceinline__ u64 ldg64(const void* p) {
   return (u64)__ldg(reinterpret_cast<const i64*>(p));
 }
+// streaming column reads: no L1 allocation, so L1 keeps the small
+// dimension structures (key bitmaps, join tables) the probes hit.
+// (asm volatile: these sit under validity predicates and must not be hoisted
+// speculatively past them)
+__device__ __forceinline__ u64 ldg64_stream(const void* p) {
+  u64 v;
+  asm volatile("ld.global.nc.L1::no_allocate.b64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+// probe-side reads of small, hot structures: keep in L1
+__device__ __forceinline__ u64 ldg64_keep(const void* p) {
+  u64 v;
+  asm volatile("ld.global.nc.L1::evict_last.b64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void ldg128_keep(const void* p, u64& a, u64& b) {
+  asm volatile("ld.global.nc.L1::evict_last.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+}
 __device__ __forceinline__ void ldg128(const void* p, u64& a, u64& b) {
   longlong2 v = __ldg(reinterpret_cast<const longlong2*>(p));
   a = (u64)v.x;

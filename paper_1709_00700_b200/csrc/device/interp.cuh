@@ -142,7 +142,7 @@ __device__ __forceinline__ void load_column(const KParams& kp, int slot, const B
   const int64_t* __restrict__ c = reinterpret_cast<const int64_t*>(kp.p.d_columns[slot]);
   if constexpr (ACCESS == kGather) {  // compacted rows: gathers
 #pragma unroll
-    for (int j = 0; j < R; ++j) v[j] = ((b.valid >> j) & 1u) ? ldg64(c + b.row(j)) : 0ull;
+    for (int j = 0; j < R; ++j) v[j] = ((b.valid >> j) & 1u) ? ldg64_stream(c + b.row(j)) : 0ull;
   } else if constexpr (ACCESS == HAWK_COALESCED) {
     if (b.stage) {  // staged tile in shared memory
       const int64_t* t = b.stage + (size_t)kp.stage_of[slot] * b.B * R;
@@ -150,7 +150,7 @@ __device__ __forceinline__ void load_column(const KParams& kp, int slot, const B
       for (int j = 0; j < R; ++j) v[j] = (u64)t[b.sidx(j)];
     } else {        // unstaged: warp-coalesced 8-byte loads
 #pragma unroll
-      for (int j = 0; j < R; ++j) v[j] = ((b.valid >> j) & 1u) ? ldg64(c + b.row(j)) : 0ull;
+      for (int j = 0; j < R; ++j) v[j] = ((b.valid >> j) & 1u) ? ldg64_stream(c + b.row(j)) : 0ull;
     }
   } else if (b.valid == (1u << R) - 1u) {
 #pragma unroll

@@ -733,6 +733,17 @@ __device__ __forceinline__ void pipeline_body(const KParams& kp) {
 #pragma unroll
       for (int j = 0; j < R; ++j) rid[j] = (u64)(b.row(j) + p.row_offset);
       table_insert_rows<IMPL, HFN, R>(p.sink_table, key, rid, alive, kp.d_flags);
+      if (p.sink_table.d_bits != nullptr) {  // exact key bitmap for filter-only probes
+        unsigned long long* bits = reinterpret_cast<unsigned long long*>(p.sink_table.d_bits);
+        const u64 words = ((u64)p.sink_table.bits_span + 63ull) >> 6;
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          const u64 r = key[j] - (u64)p.sink_table.bits_lo;
+          if (((alive >> j) & 1u) && r < (u64)p.sink_table.bits_span)
+            for (int c = 0; c < p.sink_table.bits_copies; ++c)
+              atomicOr(bits + c * words + (r >> 6), 1ull << (r & 63));
+        }
+      }
     }
   };
 

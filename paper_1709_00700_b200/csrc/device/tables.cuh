@@ -47,7 +47,7 @@ __device__ __forceinline__ void table_find_rows(const hawk_table& t, const u64 (
 #pragma unroll
   for (int j = 0; j < R; ++j) {
     pos[j] = hash_slot<HFN>(key[j], t.seed[0], t.log2_capacity);
-    if ((act >> j) & 1u) ldg128(s + 2 * pos[j], k0[j], v0[j]);
+    if ((act >> j) & 1u) ldg128_keep(s + 2 * pos[j], k0[j], v0[j]);
     else k0[j] = kEmpty, v0[j] = 0;
   }
   if (IMPL == HAWK_LINEAR_PROBING) {
@@ -70,7 +70,7 @@ __device__ __forceinline__ void table_find_rows(const hawk_table& t, const u64 (
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       const u64 i = hash_slot<HFN>(key[j], t.seed[1], t.log2_capacity);
-      if ((act >> j) & 1u) ldg128(s + 2 * ((u64)t.capacity + i), k1[j], v1[j]);
+      if ((act >> j) & 1u) ldg128_keep(s + 2 * ((u64)t.capacity + i), k1[j], v1[j]);
       else k1[j] = kEmpty, v1[j] = 0;
     }
 #pragma unroll

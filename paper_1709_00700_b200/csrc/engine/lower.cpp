@@ -302,9 +302,27 @@ void reorder_probes(LoweredProgram& lp, const std::vector<double>& match_prob) {
   for (int i = 0; i < p.nproject; ++i) remap(p.project[i]);
 }
 
+// A probe is a pure semi-join when no operand of the program reads its build
+// payload (TPC-H/SSB filter joins such as SSB Q4.1's supplier and part).
+static void mark_filter_only_probes(hawk_pipeline& p) {
+  bool used[HAWK_MAX_PROBES] = {};
+  auto see = [&](const hawk_operand& o) {
+    if (o.kind == HAWK_OPND_PAYLOAD && o.probe >= 0 && o.probe < HAWK_MAX_PROBES) used[o.probe] = true;
+  };
+  for (int i = 0; i < p.nprobe; ++i) see(p.probe[i].key);
+  for (int i = 0; i < p.npost; ++i) see(p.post[i].lhs), see(p.post[i].rhs);
+  for (int i = 0; i < p.nfilter; ++i) see(p.filter[i].lhs), see(p.filter[i].rhs);
+  for (int i = 0; i < p.narith; ++i) see(p.arith[i].lhs), see(p.arith[i].rhs);
+  for (int i = 0; i < p.nkeys; ++i) see(p.keys[i]);
+  for (int i = 0; i < p.naggs; ++i) see(p.aggs[i].input);
+  for (int i = 0; i < p.nproject; ++i) see(p.project[i]);
+  for (int i = 0; i < p.nprobe; ++i) p.probe[i].filter_only = used[i] ? 0 : 1;
+}
+
 LoweredProgram lower_program(const PipelineProgram& program, const PipelineSet& set) {
   Lowerer l(program, set);
   l.run();
+  mark_filter_only_probes(l.out.pipe);
   return l.out;
 }
 

@@ -1,3 +1,4 @@
+timeout 1800 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
 for q in tpch_q1 tpch_q6 ssb_q11 ssb_q41 tpch_q3; do
   timeout 900 python bench.py --query $q > gpurun_out/bench_$q.json 2> gpurun_out/bench_$q.err || tail -3 gpurun_out/bench_$q.err
 done
