@@ -238,6 +238,7 @@ typedef struct hawk_output {
   int64_t stride;   /* PROJECT: column stride in elements */
   int32_t width;    /* words per row */
   int32_t flags;    /* HAWK_FLAG_* raised by the kernels */
+  const int64_t* h_values; /* AGGREGATE: host copy of d_values (valid until the next launch) */
 } hawk_output;
 
 enum {

@@ -37,6 +37,7 @@ struct hawk_ctx {
   // control block: [0] flags (int) [1] counter (unsigned) [2] cursor [3] total
   u64* d_ctrl = nullptr;
   u64* d_final = nullptr;  // HAWK_MAX_AGGS
+  u64* h_readback = nullptr;  // pinned: ctrl words + AGGREGATE accumulators, one D2H
   u64* d_partials = nullptr;
   size_t partials_cap = 0;
   int64_t* d_offsets = nullptr;
@@ -436,6 +437,7 @@ int32_t hawk_b200_ctx_create(int32_t device, hawk_ctx** out) {
   HK_TRY(cudaMalloc(&ctx->d_ctrl, 64));
   HK_TRY(cudaMemset(ctx->d_ctrl, 0, 64));
   HK_TRY(cudaMalloc(&ctx->d_final, HAWK_MAX_AGGS * 8));
+  HK_TRY(cudaMallocHost(&ctx->h_readback, (4 + HAWK_MAX_AGGS) * 8));
   HK_TRY(cudaEventCreate(&ctx->ev0));
   HK_TRY(cudaEventCreate(&ctx->ev1));
   *out = ctx;
@@ -449,6 +451,7 @@ int32_t hawk_b200_ctx_destroy(hawk_ctx* ctx) {
   for (void* p : {(void*)ctx->d_ctrl, (void*)ctx->d_final, (void*)ctx->d_partials,
                   (void*)ctx->d_offsets, (void*)ctx->d_out, (void*)ctx->d_groups, ctx->d_flush})
     if (p) cudaFree(p);
+  if (ctx->h_readback) cudaFreeHost(ctx->h_readback);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
   cudaStreamDestroy(ctx->stream);
@@ -913,8 +916,7 @@ int32_t hawk_b200_run_pipeline(hawk_ctx* ctx, const hawk_pipeline* pipe, const h
   unsigned* d_counter = reinterpret_cast<unsigned*>(ctx->d_ctrl + 1);
   u64* d_cursor = ctx->d_ctrl + 2;
   int64_t* d_total = reinterpret_cast<int64_t*>(ctx->d_ctrl + 3);
-  HK_TRY(cudaMemsetAsync(d_flags, 0, 4, ctx->stream));
-  HK_TRY(cudaMemsetAsync(d_cursor, 0, 16, ctx->stream));
+  HK_TRY(cudaMemsetAsync(ctx->d_ctrl, 0, 32, ctx->stream));  // flags, ticket, cursor, total
 
   hk::KParams kp;
   std::memset(&kp, 0, sizeof kp);
@@ -1048,8 +1050,13 @@ int32_t hawk_b200_run_pipeline(hawk_ctx* ctx, const hawk_pipeline* pipe, const h
   }
   HK_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
   const double t_launch = trace ? us_since(t_start) : 0.0;
-  u64 ctrl[4];
-  HK_TRY(cudaMemcpyAsync(ctrl, ctx->d_ctrl, sizeof ctrl, cudaMemcpyDeviceToHost, ctx->stream));
+  // one synchronising read-back: the control words and, for AGGREGATE, the
+  // accumulators themselves (pinned)
+  u64* ctrl = ctx->h_readback;
+  HK_TRY(cudaMemcpyAsync(ctrl, ctx->d_ctrl, 4 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (p.sink == HAWK_SINK_AGGREGATE && p.naggs > 0)
+    HK_TRY(cudaMemcpyAsync(ctrl + 4, ctx->d_final, (size_t)p.naggs * 8, cudaMemcpyDeviceToHost,
+                           ctx->stream));
   HK_TRY(cudaStreamSynchronize(ctx->stream));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
@@ -1062,6 +1069,7 @@ int32_t hawk_b200_run_pipeline(hawk_ctx* ctx, const hawk_pipeline* pipe, const h
   switch (p.sink) {
     case HAWK_SINK_AGGREGATE:
       out->d_values = reinterpret_cast<int64_t*>(ctx->d_final);
+      out->h_values = reinterpret_cast<const int64_t*>(ctrl + 4);
       out->rows = 1;
       out->width = p.naggs;
       out->stride = p.naggs;
