@@ -453,7 +453,7 @@ Value decode_value(const PipelineSet& set, const OutputColumn& oc, int64_t raw) 
 // 1.2M groups: a single thread reading the DMA-written rows is memory bound).
 template <typename F>
 void parallel_rows(int64_t n, F&& f) {
-  const int64_t per_thread = 1 << 17;
+  const int64_t per_thread = 1 << 15;
   const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
   const int T = static_cast<int>(std::min<int64_t>(std::min(hw, 16), (n + per_thread - 1) / per_thread));
   if (T <= 1) {
