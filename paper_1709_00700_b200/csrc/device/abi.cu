@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "hawk_b200.h"
+#include "hawk_b200_cross.h"
 #include "hawk_gen.h"
 #include "kernels_misc.cuh"
 #include "jit.cuh"
@@ -382,6 +383,22 @@ int32_t prepare(hawk_ctx* ctx, const hawk_pipeline& pipe, const hawk_variant& v,
 }
 
 bool valid_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// CROSS_JOIN pair space (hawk_b200_cross.h): one column, driver-major, two
+// rows per thread per step so each warp writes 512 contiguous bytes
+__global__ void cross_expand_kernel(const int64_t* __restrict__ src, int64_t n_aux, int32_t side,
+                                    int64_t n, int64_t padded, int64_t* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); i < padded; i += 2 * stride) {
+    int64_t v[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int64_t r = i + k;
+      v[k] = r < n ? src[side == 0 ? r / n_aux : r % n_aux] : 0;
+    }
+    *reinterpret_cast<longlong2*>(out + i) = make_longlong2(v[0], v[1]);
+  }
+}
 
 }  // namespace
 
@@ -1100,3 +1117,18 @@ int32_t hawk_b200_run_pipeline(hawk_ctx* ctx, const hawk_pipeline* pipe, const h
 }
 
 }  // extern "C"
+
+// ---- CROSS_JOIN ---------------------------------------------------------------------
+
+int32_t hawk_b200_cross_expand(hawk_ctx* ctx, const int64_t* d_src, int64_t n_driver,
+                               int64_t n_aux, int32_t side, int64_t* d_out) {
+  if (!ctx || !d_out || n_driver < 0 || n_aux < 0 || (side != 0 && side != 1)) return HAWK_ERR_ARGUMENT;
+  const int64_t n = n_driver * n_aux;
+  if (n > 0 && !d_src) return HAWK_ERR_ARGUMENT;
+  const int64_t padded = std::max<int64_t>(64, (n + 63) / 64 * 64);
+  cudaSetDevice(ctx->device);
+  const int64_t blocks = std::min<int64_t>((int64_t)ctx->sms * 8, (padded / 2 + 255) / 256);
+  cross_expand_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(d_src, n_aux, side, n, padded, d_out);
+  HK_TRY(cudaGetLastError());
+  return HAWK_OK;
+}

@@ -16,6 +16,7 @@
 #include "hawk/sql/parser.hpp"
 #include "hawk_b200_engine.hpp"
 #include "hawk_gen.h"
+#include "hawk_b200_cross.h"
 
 namespace hawk::b200 {
 
@@ -675,9 +676,156 @@ struct PhaseTrace {
   }
 };
 
+// CROSS_JOIN (planner_pipelines.cpp:337-352, oracle
+// planner_reference.cpp:188-203). The reference nests a loop over the
+// auxiliary table inside the driver loop; here the terminal pipeline's
+// LOOP(driver) ... CROSS_JOIN(aux) becomes LOOP over a device-materialised
+// pair table of n_driver x n_aux rows in driver-major order (one
+// hawk_b200_cross_expand per referenced column), so every op after it —
+// aux filters, probes keyed by aux columns, residual cross-table filters,
+// aggregation — runs unchanged on the fused kernel skeleton. Driver-side ops
+// before the CROSS_JOIN are evaluated once per pair, which is the same
+// result. Only the terminal pipeline can carry a CROSS_JOIN: build sides are
+// a scan (+select) of one table (sql_parser.cpp:607-611).
+struct CrossExpansion {
+  PipelineSet set;
+  std::vector<std::string> device_tables;  // pair tables to free after the run
+};
+
+static bool has_cross_join(const PipelineProgram& p) {
+  for (const PipelineOp& op : p.ops)
+    if (op.kind == PipelineOpKind::CrossJoin) return true;
+  return false;
+}
+
+static void expand_cross_joins(Engine::Impl& I, const PipelineSet& in, CrossExpansion& x) {
+  x.set = in;
+  for (std::size_t i = 0; i < in.pipelines.size(); ++i)
+    if (static_cast<int>(i) != in.terminal && has_cross_join(in.pipelines[i]))
+      throw Unsupported("CROSS_JOIN outside the terminal pipeline");
+  PipelineProgram& prog = x.set.pipelines[static_cast<std::size_t>(in.terminal)];
+  static int serial = 0;
+  for (;;) {
+    std::size_t k = 0;
+    while (k < prog.ops.size() && prog.ops[k].kind != PipelineOpKind::CrossJoin) ++k;
+    if (k == prog.ops.size()) break;
+    const int D = prog.driver_table, A = prog.ops[k].table;
+    const int X = static_cast<int>(x.set.tables.size());
+    const Table& dcat = *x.set.tables.at(static_cast<std::size_t>(D));
+    const Table& acat = *x.set.tables.at(static_cast<std::size_t>(A));
+    const int nd_cols = static_cast<int>(dcat.column_count());
+    Schema schema;
+    for (std::size_t c = 0; c < dcat.column_count(); ++c)
+      schema.push_back({"d." + dcat.column_name(c), dcat.column(c).kind()});
+    for (std::size_t c = 0; c < acat.column_count(); ++c)
+      schema.push_back({"a." + acat.column_name(c), acat.column(c).kind()});
+    const std::string name = "__cross" + std::to_string(++serial) + ":" + dcat.name() + "*" + acat.name();
+    auto cat = std::make_shared<Table>(name, schema);
+    cat->finalize();
+    x.set.tables.push_back(cat);
+
+    // reroute: driver columns keep their index, aux columns follow them
+    auto fix = [&](OpAttr& a) {
+      if (a.route == AttrRoute::Driver && a.table == D) {
+        a.table = X;
+      } else if (a.route == AttrRoute::CrossAux && a.table == A) {
+        a.route = AttrRoute::Driver;
+        a.table = X;
+        a.column += nd_cols;
+        a.aux_op = -1;
+      }
+    };
+    auto fix_operand = [&](OpOperand& o) {
+      if (o.kind == OpOperand::Kind::Attr) fix(o.attr);
+    };
+    for (PipelineOp& op : prog.ops) {
+      for (OpComparison& c : op.predicate) {
+        fix(c.lhs);
+        fix_operand(c.rhs);
+      }
+      for (OpAttr& a : op.keys) fix(a);
+      for (OpAttr& a : op.payload) fix(a);
+      for (OpAttr& a : op.attrs) fix(a);
+      fix_operand(op.arith_lhs);
+      fix_operand(op.arith_rhs);
+      for (OpAggregate& g : op.aggregates) fix_operand(g.input);
+    }
+    prog.ops.erase(prog.ops.begin() + static_cast<std::ptrdiff_t>(k));
+    prog.ops.front().table = X;
+    prog.driver_table = X;
+
+    // materialise the referenced columns of the pair table
+    std::vector<bool> used(schema.size(), false);
+    auto mark = [&](const OpAttr& a) {
+      if (a.route == AttrRoute::Driver && a.table == X) used.at(static_cast<std::size_t>(a.column)) = true;
+    };
+    for (const PipelineOp& op : prog.ops) {
+      for (const OpComparison& c : op.predicate) {
+        mark(c.lhs);
+        if (c.rhs.kind == OpOperand::Kind::Attr) mark(c.rhs.attr);
+      }
+      for (const OpAttr& a : op.keys) mark(a);
+      for (const OpAttr& a : op.payload) mark(a);
+      for (const OpAttr& a : op.attrs) mark(a);
+      if (op.arith_lhs.kind == OpOperand::Kind::Attr) mark(op.arith_lhs.attr);
+      if (op.arith_rhs.kind == OpOperand::Kind::Attr) mark(op.arith_rhs.attr);
+      for (const OpAggregate& g : op.aggregates)
+        if (g.input.kind == OpOperand::Kind::Attr) mark(g.input.attr);
+    }
+    const DeviceTable& dd = I.device_table(x.set, D);
+    const DeviceTable& ad = I.device_table(x.set, A);
+    DeviceTable dt;
+    dt.name = name;
+    dt.rows = dd.rows * ad.rows;
+    dt.catalog = cat;
+    const size_t bytes = static_cast<size_t>(padded_rows(dt.rows)) * 8;
+    x.device_tables.push_back(name);
+    I.tables[name] = DeviceTable{name, 0, 0, {}, cat};  // freed by the caller even on error
+    for (std::size_t c = 0; c < schema.size(); ++c) {
+      if (!used[c]) continue;
+      const bool aux = static_cast<int>(c) >= nd_cols;
+      const int src_col = aux ? static_cast<int>(c) - nd_cols : static_cast<int>(c);
+      const DeviceColumn& src = I.device_column(x.set, aux ? A : D, src_col);
+      DeviceColumn col;
+      col.name = schema[c].name;
+      col.kind = src.kind;
+      col.distinct = src.distinct;
+      void* p = nullptr;
+      check(hawk_b200_alloc(I.ctx, bytes, &p), "cross-join column allocation");
+      col.d_data = static_cast<int64_t*>(p);
+      I.tables[name].columns.push_back(col);
+      check(hawk_b200_cross_expand(I.ctx, src.d_data, dd.rows, ad.rows, aux ? 1 : 0, col.d_data),
+            "cross-join expansion");
+    }
+    I.tables[name].rows = dt.rows;
+  }
+}
+
 static QueryRun run_query(Engine& e, Engine::Impl& I, const PipelineSet& set,
                           const std::vector<VariantConfiguration>& configs, ExecutionMetrics* m,
                           bool partial) {
+  if (set.terminal >= 0 && static_cast<std::size_t>(set.terminal) < set.pipelines.size() &&
+      has_cross_join(set.pipelines[static_cast<std::size_t>(set.terminal)])) {
+    require_device(e.ctx());
+    CrossExpansion x;
+    auto cleanup = [&]() {
+      for (const std::string& n : x.device_tables) {
+        auto it = I.tables.find(n);
+        if (it == I.tables.end()) continue;
+        I.free_table(it->second);
+        I.tables.erase(it);
+      }
+    };
+    try {
+      expand_cross_joins(I, set, x);
+      QueryRun r = run_query(e, I, x.set, configs, m, partial);
+      cleanup();
+      return r;
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+  }
   const auto t0 = std::chrono::steady_clock::now();
   PhaseTrace trace;
   trace.ctx = e.ctx();

@@ -19,6 +19,13 @@ def test_b200_library_exports_header():
     assert not missing, missing
 
 
+def test_b200_library_exports_cross_header():
+    lib = _native.b200()
+    names = _native.declared_symbols(os.path.join(ROOT, "include", "hawk_b200_cross.h"))
+    assert names == ["hawk_b200_cross_expand"]
+    assert hasattr(lib, names[0])
+
+
 def test_engine_library_exports_header():
     lib = _native.engine()
     names = _native.declared_symbols(os.path.join(ROOT, "include", "hawk_b200_engine.h"))

@@ -17,7 +17,7 @@ from oracle_bridge import OraError, OraTable
 from paper_1709_00700_b200 import (DuplicateKey, EmptyAggregate, Engine, _native)
 from paper_1709_00700_b200 import datagen as dg
 from paper_1709_00700_b200 import queries as Q
-from paper_1709_00700_b200.engine import INT64, Column
+from paper_1709_00700_b200.engine import FLOAT64, INT64, Column
 
 pytestmark = pytest.mark.gpu
 
@@ -340,3 +340,79 @@ def test_sf10_bench_queries_match_port(key):
                     assert abs(x - y) <= 1e-9 * max(1.0, abs(x), abs(y)), (key, cfg, a, b)
     finally:
         e.close()
+
+
+# ---- CROSS_JOIN (planner_pipelines.cpp:337-352) -------------------
+
+CROSS_QUERIES = [
+    # aux filter + driver filter, non-grouped
+    "select count(*), sum(lo_quantity*a_w) from xa, lineorder where a_w < 5 and lo_quantity < 10",
+    # group key from the auxiliary side
+    "select a_k, sum(lo_revenue), count(*) from xa, lineorder where lo_discount < 3 group by a_k",
+    # residual cross-table comparison (a post-join filter)
+    "select count(*) from xa, lineorder where lo_quantity < a_w",
+    # mixed int x double arithmetic over an aux column
+    "select sum(lo_revenue*a_f) from xa, lineorder where lo_quantity < 20",
+    # cross join next to a hash join
+    "select count(*), sum(lo_revenue) from supplier, xa, lineorder "
+    "where lo_suppkey = s_suppkey and s_region = 'ASIA' and a_w > 1",
+    # projection of driver and aux columns
+    "select lo_linenumber, a_k from xa, lineorder where lo_quantity < 2",
+    # empty auxiliary side after its filter
+    "select count(*) from xa, lineorder where a_w > 100",
+]
+
+
+@pytest.fixture(scope="module")
+def cross(micro):
+    engine, db = micro
+    cols = [Column("a_k", INT64, np.array([3, 1, 4, 1, 5, 9, 2], np.int64)),
+            Column("a_w", INT64, np.array([2, 7, 1, 8, 2, 8, 1], np.int64)),
+            Column("a_f", FLOAT64, np.array([0.5, 1.25, -2.0, 3.5, 0.0, 1e-3, 7.0]))]
+    engine.put_table("xa", cols)
+    db.add(OraTable.from_columns("xa", cols))
+    return engine, db
+
+
+@pytest.mark.parametrize("jit", [1, 0], ids=["compiled", "interpreted"])
+@pytest.mark.parametrize("qi", range(len(CROSS_QUERIES)))
+def test_cross_join_parity(cross, qi, jit):
+    engine, db = cross
+    sql = CROSS_QUERIES[qi]
+    expected = db.execute(sql)
+    engine.set_option("jit", jit)
+    try:
+        for cfg in CONFIGS:
+            diff = harness.compare(expected, engine.run(sql, cfg))
+            assert diff is None, f"{sql} [{cfg}]: {diff}"
+    finally:
+        engine.set_option("jit", 0)
+
+
+@pytest.mark.parametrize("n_driver,n_aux", [(0, 5), (5, 0), (1, 1), (1000, 7), (3, 4096)])
+def test_cross_expand_kernel(engine, n_driver, n_aux):
+    # one column of the driver-major pair space, both sides, padding zeroed
+    lib = _native.b200()
+    ctx = engine.ctx
+    rng = np.random.default_rng(n_driver * 7 + n_aux)
+    src_d = rng.integers(-2**62, 2**62, size=max(n_driver, 1), dtype=np.int64)
+    src_a = rng.integers(-2**62, 2**62, size=max(n_aux, 1), dtype=np.int64)
+    n = n_driver * n_aux
+    padded = max(64, (n + 63) // 64 * 64)
+    for side, src, want in ((0, src_d, np.repeat(src_d[:n_driver], n_aux)),
+                            (1, src_a, np.tile(src_a[:n_aux], n_driver))):
+        d_src, d_out = C.c_void_p(), C.c_void_p()
+        assert lib.hawk_b200_alloc(ctx, src.nbytes, C.byref(d_src)) == 0
+        assert lib.hawk_b200_alloc(ctx, padded * 8, C.byref(d_out)) == 0
+        assert lib.hawk_b200_memcpy_h2d(ctx, d_src, src.ctypes.data, src.nbytes) == 0
+        assert lib.hawk_b200_memset(ctx, d_out, 0xff, padded * 8) == 0
+        assert lib.hawk_b200_cross_expand(ctx, d_src, C.c_int64(n_driver), C.c_int64(n_aux),
+                                          side, d_out) == 0
+        out = np.empty(padded, np.int64)
+        assert lib.hawk_b200_memcpy_d2h(ctx, out.ctypes.data, d_out, out.nbytes) == 0
+        assert np.array_equal(out[:n], want)
+        assert not out[n:].any()
+        lib.hawk_b200_free(ctx, d_src)
+        lib.hawk_b200_free(ctx, d_out)
+    assert lib.hawk_b200_cross_expand(ctx, None, C.c_int64(1), C.c_int64(1), 0, d_out) != 0
+    assert lib.hawk_b200_cross_expand(ctx, d_src, C.c_int64(1), C.c_int64(1), 2, d_out) != 0
