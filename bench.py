@@ -52,7 +52,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-rows", type=int, default=4_000_000)
     ap.add_argument("--prefetch", type=int, default=None, help="TMA pipeline depth (pass tiles)")
-    ap.add_argument("--stage", type=int, default=1, help="1: TMA-staged pass tiles (coalesced)")
+    ap.add_argument("--stage", type=int, default=0,
+                    help="1: TMA-staged pass tiles (coalesced); 0: coalesced 128-bit loads from HBM")
     ap.add_argument("--min-ctas", type=int, default=None,
                     help="compiled programs: __launch_bounds__ minimum CTAs per SM")
     ap.add_argument("--compact", type=int, default=None,

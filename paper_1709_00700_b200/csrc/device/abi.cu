@@ -26,14 +26,18 @@ struct hawk_ctx {
   int smem_optin = 227 * 1024;
   int prefetch_passes = 2;  // COALESCED: TMA pipeline depth in pass tiles
   int l2_distance = 0;      // COALESCED, unstaged: L2 bulk-prefetch distance in passes
-  int pass_sync = 1;        // COALESCED, unstaged: CTA barrier after every pass tile
+  int pass_sync = 0;        // COALESCED, unstaged: CTA barrier after every pass tile
   int stage_probes = 0;     // COALESCED pipelines with probes: TMA staging + barrier too
   int dense_keys = 1;       // HAGG_LOCAL compiled: dense key-index lookaside when provided
   int compact = 1;          // compiled, branched: compact live rows after the first probe
   int min_ctas = 0;         // compiled: __launch_bounds__ min CTAs/SM override (0 = default)
   int priv_groups = 64;     // HAGG_LOCAL: groups with thread-private accumulators
   int jit = 0;              // compiled programs (jit.cu) instead of the interpreter
-  int stage = 1;            // COALESCED: stage pass tiles in smem with TMA
+  // COALESCED: stage pass tiles in smem with TMA. Off by default since the
+  // private-accumulator group-by: TPC-H Q1 SF10 terminal 0.744 -> 0.712 ms
+  // unstaged without the pass barrier, TPC-H Q6 unchanged (0.0343 ms both;
+  // profiles/README.md, r01 staging A/B)
+  int stage = 0;
   int64_t l2_bytes = 0;
   // control block: [0] flags (int) [1] counter (unsigned) [2] cursor [3] total
   u64* d_ctrl = nullptr;
@@ -322,8 +326,8 @@ int32_t prepare(hawk_ctx* ctx, const hawk_pipeline& pipe, const hawk_variant& v,
   // per-pass CTA barrier: probe latency varies per warp (random L2/HBM slot
   // loads), and a barrier per pass tile would make every warp wait for the
   // slowest one (measured: SSB Q4.1 SF10 1.58 -> 1.30 ms, TPC-H Q3 terminal
-  // 1.02 -> 0.79 ms). Scan-only pipelines keep TMA staging / the barrier,
-  // which keeps a CTA's warps on one tile (TPC-H Q1 1.36 -> 1.21 ms).
+  // 1.02 -> 0.79 ms). Scan-only pipelines stage with TMA / keep the barrier
+  // only when the stage / pass_sync options ask for it.
   const bool probe_free = pipe.nprobe > 0 && !ctx->stage_probes;
   if (probe_free) kp.pass_sync = 0;
   if (!ctx->stage || probe_free) {  // coalesced loads straight from HBM, no TMA staging

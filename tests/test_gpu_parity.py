@@ -56,6 +56,25 @@ def test_micro_queries_all_strategies(micro, cfg, jit):
     engine.set_option("jit", 0)
 
 
+@pytest.mark.parametrize("jit", [1, 0], ids=["compiled", "interpreted"])
+def test_micro_queries_tma_staged(micro, jit):
+    # the TMA-staged pass tiles with a per-pass CTA barrier (option stage=1,
+    # pass_sync=1) are a variant point next to the default HBM-direct loads
+    engine, db = micro
+    engine.set_option("jit", jit)
+    engine.set_option("stage", 1)
+    engine.set_option("pass_sync", 1)
+    try:
+        for cfg in CONFIGS:
+            for name, sql in harness.MICRO:
+                diff = harness.compare(db.execute(sql), engine.run(sql, cfg))
+                assert diff is None, f"{name} [{cfg}] staged: {diff}"
+    finally:
+        engine.set_option("stage", 0)
+        engine.set_option("pass_sync", 0)
+        engine.set_option("jit", 0)
+
+
 @pytest.mark.parametrize("jit,stride", [(0, 1), (1, 8)], ids=["interpreted-all", "compiled-sample"])
 def test_listing2_full_projection_space(micro, jit, stride):
     engine, db = micro
