@@ -36,7 +36,7 @@ struct hawk_ctx {
   // COALESCED: stage pass tiles in smem with TMA. Off by default since the
   // private-accumulator group-by: TPC-H Q1 SF10 terminal 0.744 -> 0.712 ms
   // unstaged without the pass barrier, TPC-H Q6 unchanged (0.0343 ms both;
-  // profiles/README.md, r01 staging A/B)
+  // profiles/ab_r01_staging.txt)
   int stage = 0;
   int64_t l2_bytes = 0;
   // control block: [0] flags (int) [1] counter (unsigned) [2] cursor [3] total
