@@ -126,3 +126,25 @@ def test_port_matches_reference_execute(key, sf):
 def test_port_thread_count_independent():
     # SPEC.md:549 determinism across worker counts
     assert port_rows("tpch_q1", 0.01, 7, threads=1) == port_rows("tpch_q1", 0.01, 7, threads=8)
+
+
+def test_cross_join_oracle_closed_form():
+    # the reference's CROSS_JOIN pairs every probe-side row
+    # with every auxiliary row (planner_reference.cpp:188-203), so a count and
+    # a product-sum over the pairs factor into per-side numpy reductions
+    from oracle_bridge import OraTable
+    from paper_1709_00700_b200.engine import INT64, Column
+    tables = harness.micro_tables(20000, 5)
+    db = harness.oracle_db(tables)
+    a_w = np.array([2, 7, 1, 8, 2, 8, 1], np.int64)
+    db.add(OraTable.from_columns("xa", [Column("a_k", INT64, np.arange(7, dtype=np.int64)),
+                                        Column("a_w", INT64, a_w)]))
+    lo = {c.name: np.asarray(c.values) for c in tables[0].columns()}
+    q = lo["lo_quantity"]
+    res = db.execute("select count(*), sum(lo_quantity*a_w) from xa, lineorder "
+                     "where a_w < 5 and lo_quantity < 10")
+    cols = {c.name: np.asarray(c.values) for c in res.columns()}
+    vals = sorted(int(v[0]) for v in cols.values())
+    want = sorted([int((q < 10).sum()) * int((a_w < 5).sum()),
+                   int(q[q < 10].sum()) * int(a_w[a_w < 5].sum())])
+    assert vals == want
