@@ -1,13 +1,20 @@
-"""Benchmark: input tuples/s and HBM roofline fraction of a BASELINE query on
-1..8 B200s (BASELINE.json metric), beside the reference's CPU path.
+"""Benchmark: input tuples/s and HBM roofline fraction of the BASELINE queries
+on 1..8 B200s (BASELINE.json metric), beside the reference's CPU path.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--query tpch_q1] [--sf 10]
-                  [--config "<proj>;<agg>"] [--impl ours|reference]
+                  [--config "<proj>;<agg>"] [--impl ours|reference] [--no-per-query]
 
 One step = one execution of every pipeline of the query over the resident
 synthetic tables (fact table row-sharded over ranks, weak scaling: each rank
 holds an SF-sized shard of an N*SF table). Printed: one JSON line (rank 0).
-Default workload: TPC-H Q1 at SF10 (BASELINE.json configs[1]).
+Headline workload: TPC-H Q1 at SF10 (BASELINE.json configs[1]); at N=1 the
+line also carries a `per_query` block with every BASELINE configuration at
+its own scale factor (Q6 SF1, Q1 SF10, SSB Q1.1 SF10, SSB Q4.1 SF100,
+TPC-H Q3 SF100).
+
+--impl reference: the reference's own CPU path (reference_execute, compiled
+unmodified into oracle/_ref) over the same whole workload on every host core
+(tests/ref_sharded.py), rank 0 only.
 """
 from __future__ import annotations
 
@@ -25,7 +32,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "input tuples/sec & HBM GB/s (roofline frac) per TPC-H/SSB query, 1/2/4/8 B200"
 
-# learned/selected variant per query (see DESIGN.md §learner; --config overrides)
+# learned/selected variant per query (see DESIGN.md §8; --config overrides)
 DEFAULT_CONFIG = {
     "tpch_q6": "single_pass/sequential/branched/u=2;global_hash/sequential/branched/linear_probing/multiply_shift/wg=256/u=2",
     "tpch_q1": "single_pass/coalesced/branched;local_hash/coalesced/predicated/linear_probing/murmur/wg=256/ht=8",
@@ -33,7 +40,9 @@ DEFAULT_CONFIG = {
     "ssb_q41": "single_pass/coalesced/branched;global_hash/coalesced/branched/linear_probing/multiply_shift/wg=256",
     "tpch_q3": "single_pass/coalesced/branched/u=4;global_hash/coalesced/branched/linear_probing/multiply_shift/wg=64",
 }
-DEFAULT_SF = {"tpch_q6": 1.0, "tpch_q1": 10.0, "ssb_q11": 10.0, "ssb_q41": 10.0, "tpch_q3": 10.0}
+# BASELINE.json configs: the scale factor each query is quoted at
+BASELINE_SF = {"tpch_q6": 1.0, "tpch_q1": 10.0, "ssb_q11": 10.0, "ssb_q41": 100.0, "tpch_q3": 100.0}
+DEFAULT_SF = BASELINE_SF
 WORKLOAD_NAME = {"tpch_q6": "TPC-H Q6", "tpch_q1": "TPC-H Q1", "ssb_q11": "SSB Q1.1",
                  "ssb_q41": "SSB Q4.1", "tpch_q3": "TPC-H Q3"}
 
@@ -50,10 +59,12 @@ def parse():
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-sample-rows", type=int, default=4_000_000)
+    ap.add_argument("--no-per-query", action="store_true",
+                    help="N=1: skip the per_query block (every BASELINE configuration)")
+    ap.add_argument("--per-query-steps", type=int, default=10)
     ap.add_argument("--prefetch", type=int, default=None, help="TMA pipeline depth (pass tiles)")
-    ap.add_argument("--stage", type=int, default=0,
-                    help="1: TMA-staged pass tiles (coalesced); 0: coalesced 128-bit loads from HBM")
+    ap.add_argument("--stage", type=int, default=None,
+                    help="1: TMA-staged pass tiles (coalesced); 0: coalesced loads from HBM")
     ap.add_argument("--min-ctas", type=int, default=None,
                     help="compiled programs: __launch_bounds__ minimum CTAs per SM")
     ap.add_argument("--compact", type=int, default=None,
@@ -62,6 +73,8 @@ def parse():
                     help="unstaged coalesced tiles: CTA barrier after every pass (1) or not (0)")
     ap.add_argument("--l2-distance", type=int, default=None,
                     help="unstaged coalesced tiles: L2 bulk-prefetch distance (passes, 0 = off)")
+    ap.add_argument("--option", action="append", default=[],
+                    help="extra engine option name=value (hawk_b200_ctx_set_option)")
     ap.add_argument("--jit", type=int, default=1,
                     help="1: compiled programs (NVRTC), 0: the AOT interpreter instantiations")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
@@ -79,37 +92,30 @@ SWEEP = [
     "single_pass/sequential/branched;local_hash/sequential/branched/linear_probing/murmur/wg=256/ht=4",
     "single_pass/coalesced/branched;global_hash/coalesced/predicated/linear_probing/murmur/wg=256",
     "single_pass/coalesced/predicated;local_hash/coalesced/predicated/linear_probing/murmur/wg=256/ht=1",
-    "single_pass/sequential/branched;local_hash/sequential/branched/linear_probing/murmur/wg=256/ht=1",
-    "multi_pass/coalesced/branched/tm=1024;local_hash/coalesced/branched/linear_probing/murmur/wg=512/ht=1",
-    "single_pass/coalesced/branched/u=2;local_hash/coalesced/branched/linear_probing/murmur/wg=256/ht=1/u=2",
-    "single_pass/coalesced/branched/u=4;local_hash/coalesced/branched/linear_probing/murmur/wg=256/ht=1/u=4",
-    "single_pass/coalesced/branched;local_hash/coalesced/branched/cuckoo/murmur/wg=256/ht=1",
-    "single_pass/coalesced/branched;local_hash/coalesced/branched/linear_probing/multiply_shift/wg=256/ht=8",
     "single_pass/coalesced/branched;global_hash/coalesced/branched/linear_probing/murmur/wg=256",
     "single_pass/coalesced/branched;global_hash/coalesced/branched/cuckoo/murmur/wg=1024",
-    "multi_pass/coalesced/branched/tm=16384;local_hash/coalesced/branched/linear_probing/murmur/wg=1024/ht=1",
 ]
 
 
+def apply_options(engine, args):
+    engine.set_option("jit", args.jit)
+    for name, val in (("prefetch_passes", args.prefetch), ("stage", args.stage),
+                      ("l2_distance", args.l2_distance), ("pass_sync", args.pass_sync),
+                      ("compact", args.compact), ("min_ctas", args.min_ctas)):
+        if val is not None:
+            engine.set_option(name, val)
+    for o in args.option:
+        k, v = o.split("=", 1)
+        engine.set_option(k, int(v))
+
+
 def run_sweep(args):
-    import torch
     from paper_1709_00700_b200 import Engine
     from paper_1709_00700_b200 import queries as Q
     query = args.query
     sf = args.sf or DEFAULT_SF[query]
     engine = Engine(0)
-    if args.prefetch is not None:
-        engine.set_option("prefetch_passes", args.prefetch)
-    engine.set_option("jit", args.jit)
-    engine.set_option("stage", args.stage)
-    if args.l2_distance is not None:
-        engine.set_option("l2_distance", args.l2_distance)
-    if args.pass_sync is not None:
-        engine.set_option("pass_sync", args.pass_sync)
-    if args.compact is not None:
-        engine.set_option("compact", args.compact)
-    if args.min_ctas is not None:
-        engine.set_option("min_ctas", args.min_ctas)
+    apply_options(engine, args)
     load_tables(engine, query, sf, args.seed, 0, 1)
     sql = Q.BENCH[query][0]
     for cfg in (args.sweep or SWEEP):
@@ -118,6 +124,7 @@ def run_sweep(args):
                 engine.run(sql, cfg)
             ks, ws = [], []
             for _ in range(5):
+                engine.flush_l2()
                 r = engine.run(sql, cfg)
                 ks.append(r.kernel_ms)
                 ws.append(r.wall_ms)
@@ -144,13 +151,18 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def host_info() -> dict:
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from ref_sharded import cpu_model
+    return {"cpu_model": cpu_model(), "cores": os.cpu_count() or 1}
+
+
 class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
 
     def __init__(self, index: int):
         self.index = index
         self.samples = []
-        self._stop = threading.Event()
         self._proc = None
 
     def __enter__(self):
@@ -198,91 +210,121 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def algorithmic_bytes(query: str, fact_rows: int, dims: dict) -> int:
-    """scanned rows x referenced columns x 8 B (+ build inserts
-    x 16 B); dimension tables <= L2 count their scan only."""
-    from paper_1709_00700_b200 import queries as Q
-    b = fact_rows * len(Q.FACT_COLUMNS[query]) * 8
-    for rows, cols in dims.values():
-        b += rows * cols * 8
-    return b
-
-
-def dims_for(query: str, sf: float) -> dict:
+def workload_config(query: str, sf: float, world: int) -> dict:
+    """The `config` object of both arms (same workload, same keys)."""
     from paper_1709_00700_b200 import datagen as dg
-    if query == "ssb_q11":
-        return {"ddate": (dg.table_rows(dg.DDATE, sf), 2)}
-    if query == "ssb_q41":
-        return {"ddate": (dg.table_rows(dg.DDATE, sf), 2),
-                "customer": (dg.table_rows(dg.SCUSTOMER, sf), 2),
-                "supplier": (dg.table_rows(dg.SUPPLIER, sf), 2),
-                "part": (dg.table_rows(dg.PART, sf), 2)}
-    if query == "tpch_q3":
-        return {"orders": (dg.table_rows(dg.ORDERS, sf), 4), "customer": (dg.table_rows(dg.CUSTOMER, sf), 2)}
-    return {}
+    from paper_1709_00700_b200 import queries as Q
+    fact = Q.BENCH[query][2]
+    per = dg.table_rows(fact, sf)
+    cfg = {"workload": f"{WORKLOAD_NAME[query]} SF{sf * world:g}", "query": query, "sf": sf * world,
+           "fact_rows": per * world}
+    if world > 1:
+        cfg["parallelism"] = f"dp{world} (fact rows sharded, SF{sf:g} per GPU)"
+    return cfg
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the reference's own reference_execute (oracle/_ref, 1 thread)
-# on a bounded sample, and our multi-threaded restatement (oracle/port)
+# algorithmic bytes (SURVEY.md §8d) from measured selectivities
 # ---------------------------------------------------------------------------
 
-def cpu_reference_sample(query: str, sf: float, seed: int, sample_rows: int, reps: int = 1):
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from oracle_bridge import OraDb, OraTable
+# count queries giving the probe / update counts of each query's terminal
+# pipeline (run untimed through the engine itself)
+ACCOUNTING = {
+    "tpch_q3": {
+        "orders_probes": "select count(*) from lineitem where l_shipdate > 19950315",
+        "customer_probes": "select count(*) from orders, lineitem where l_orderkey = o_orderkey "
+                           "and o_orderdate < 19950315 and l_shipdate > 19950315",
+        "group_updates": "select count(*) from orders, customer, lineitem where c_mktsegment = 'BUILDING' "
+                         "and c_custkey = o_custkey and l_orderkey = o_orderkey and o_orderdate < 19950315 "
+                         "and l_shipdate > 19950315",
+    },
+}
+
+
+def query_bytes(engine, query: str, sf: float, per_rank: int, world: int, result, l2: int) -> dict:
+    """scanned rows x referenced columns x 8 B, + build inserts
+    x 16 B, + probes / group updates into tables larger than L2 x 32 B (a
+    sector). `terminal` counts the fact columns the terminal kernel streams."""
     from paper_1709_00700_b200 import datagen as dg
     from paper_1709_00700_b200 import queries as Q
-    sql, tables, fact = Q.BENCH[query]
-    db = OraDb()
-    n_fact = 0
+    _, tables, fact = Q.BENCH[query]
+    fact_bytes = per_rank * len(Q.FACT_COLUMNS[query]) * 8
+    total = fact_bytes
+    detail = {"fact_scan": fact_bytes}
+    dim_cols = {dg.DDATE: 2, dg.SCUSTOMER: 3, dg.SUPPLIER: 2, dg.PART: 2, dg.ORDERS: 4, dg.CUSTOMER: 2}
     for t in tables:
-        rows = dg.table_rows(t, sf)
-        if t == fact:
-            rows = min(rows, sample_rows)
-            n_fact = rows
-        name, cols = dg.host_table(t, sf, seed, 0, rows)
-        db.add(OraTable.from_columns(name, cols))
-    times = []
-    for _ in range(max(1, reps)):
-        t0 = time.perf_counter()
-        db.execute(sql)
-        times.append(time.perf_counter() - t0)
-    return n_fact, times
+        if t != fact:
+            b = dg.table_rows(t, sf * world) * dim_cols[t] * 8
+            detail[f"scan_{dg.SCHEMA[t][0]}"] = b
+            total += b
+    inserts = sum(p["rows_out"] for p in result.pipelines[:-1])
+    detail["build_inserts"] = inserts * 16
+    total += inserts * 16
+    if query in ACCOUNTING:
+        big = {}
+        # join tables are sized next_pow2(2 x build rows) x 16 B; the orders
+        # table exceeds L2 at every SF >= 1, the customer table from SF ~60
+        cap = lambda rows: 1 << max(4, (2 * rows - 1).bit_length())  # noqa: E731
+        big["orders_probes"] = cap(dg.table_rows(dg.ORDERS, sf * world)) * 16 > l2
+        big["customer_probes"] = cap(dg.table_rows(dg.CUSTOMER, sf * world)) * 16 > l2
+        big["group_updates"] = True
+        for k, sql in ACCOUNTING[query].items():
+            n = int(engine.run(sql, DEFAULT_CONFIG[query]).columns[0].values[0])
+            detail[k] = n * 32 if big[k] else 0
+            total += detail[k]
+    return {"terminal": fact_bytes, "whole_query": total, "detail": detail}
 
 
-def cpu_port(query: str, sf: float, seed: int, threads: int):
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from test_oracle import _port_inputs
-    from oracle_bridge import port_run
-    q, cols, n, dims, codes = _port_inputs(query, sf, seed)
-    t0 = time.perf_counter()
-    port_run(q, cols, n, dims, codes, threads, out_rows=max(1024, n // 2))
-    return n, time.perf_counter() - t0
+# ---------------------------------------------------------------------------
+# the reference arm: reference_execute over the whole workload on every core
+# ---------------------------------------------------------------------------
+
+def reference_sample_rows(query: str, sf: float, world: int) -> int | None:
+    """Whole workload when its reference_execute working set (~300 B per fact
+    row, measured) fits in half the host RAM, else a bounded sample."""
+    from paper_1709_00700_b200 import datagen as dg
+    from paper_1709_00700_b200 import queries as Q
+    rows = dg.table_rows(Q.BENCH[query][2], sf) * world
+    try:
+        avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except (ValueError, OSError):
+        avail = 64 << 30
+    cap = int(avail * 0.5 / 300)
+    return None if rows <= cap and rows <= 120_000_000 else min(cap, 60_000_000)
 
 
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    sf = args.sf or DEFAULT_SF[args.query]
-    sample = args.cpu_sample_rows
-    n_fact, _ = cpu_reference_sample(args.query, sf, args.seed, sample, reps=0 or 1)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from ref_sharded import ShardedReference
+    query = args.query
+    sf = args.sf or DEFAULT_SF[query]
+    sample = reference_sample_rows(query, sf, world)
+    ref = ShardedReference(query, sf * world, args.seed, fact_rows=sample)
     times = []
     for i in range(args.warmup + args.steps):
-        _, t = cpu_reference_sample(args.query, sf, args.seed, sample, reps=1)
+        t = ref.timed(1)[0]
         if i >= args.warmup:
-            times.append(t[0])
+            times.append(t)
     ms = statistics.mean(times) * 1e3
-    value = n_fact / (ms / 1e3)
+    value = ref.fact_rows / (ms / 1e3)
+    info = host_info()
+    cfg = workload_config(query, sf, world)
+    if sample is not None:
+        cfg = dict(cfg, fact_rows=ref.fact_rows, sample="first rows of the fact table (host RAM bound)")
+    desc = (f"reference_execute (unmodified reference sources, oracle/_ref) over {ref.fact_rows} fact rows "
+            f"of {cfg['workload']}, one row shard per host thread ({ref.shards} shards, "
+            f"{ref.threads} threads), shard results merged (SUM/COUNT add, AVG = SUM/COUNT)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": f"{WORKLOAD_NAME[args.query]} SF{sf:g}", "query": args.query, "sf": sf,
-                   "sample_fact_rows": n_fact},
-        "cpu_baseline": {"value": value, "unit": "tuples/s", "cores": 1, "kind": "reference",
-                         "sample": f"reference_execute (oracle/_ref, unmodified reference sources) over the "
-                                   f"first {n_fact} fact rows of the SF{sf:g} workload per step"},
+        "config": cfg,
+        "cpu_baseline": {"value": value, "unit": "tuples/s", "cores": ref.threads, "kind": "reference",
+                         "sample": desc, "cpu_model": info["cpu_model"], "host_cores": info["cores"],
+                         "table_build_s": ref.build_s},
         "e2e": {"value": value, "unit": "tuples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -308,6 +350,84 @@ def load_tables(engine, query: str, sf: float, seed: int, rank: int, world: int)
     return per
 
 
+def drop_tables(engine, query: str):
+    from paper_1709_00700_b200 import datagen as dg
+    from paper_1709_00700_b200 import queries as Q
+    for t in Q.BENCH[query][1]:
+        name = dg.SCHEMA[t][0]
+        if engine.table_rows(name) >= 0:
+            engine.drop(name)
+
+
+def timed_steps(engine, stream, step, steps, warmup, flush, clocks=None, world=1):
+    """W untimed steps, then K steps each bracketed by CUDA events on the
+    engine's stream. Returns (total ms, per-step results)."""
+    import torch
+    for _ in range(warmup):
+        if flush:
+            engine.flush_l2()
+        step()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    total_ms, outs = 0.0, []
+    for _ in range(steps):
+        if flush:
+            engine.flush_l2()
+        start.record(stream)
+        outs.append(step())
+        end.record(stream)
+        end.synchronize()
+        total_ms += start.elapsed_time(end)
+    torch.cuda.synchronize()
+    return total_ms, outs
+
+
+def ncu_traffic(query: str, sf: float):
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(prof)).get(f"{query}@sf{sf:g}")
+    except Exception:
+        return None
+
+
+def measure_query(engine, stream, query, sf, cfg, steps, warmup, l2, peak):
+    """One BASELINE configuration at N=1: whole-query and terminal-kernel
+    throughput with both roofline fractions (per_query block)."""
+    from paper_1709_00700_b200 import datagen as dg
+    from paper_1709_00700_b200 import queries as Q
+    sql, tables, fact = Q.BENCH[query]
+    per = load_tables(engine, query, sf, 42, 0, 1)
+    input_tuples = sum(dg.table_rows(t, sf) for t in tables)
+    r0 = engine.run(sql, cfg)
+    acct = query_bytes(engine, query, sf, per, 1, r0, l2)
+    flush = acct["whole_query"] < 4 * l2
+    total_ms, outs = timed_steps(engine, stream, lambda: engine.run(sql, cfg), steps, warmup, flush)
+    ms = total_ms / steps
+    term_ms = statistics.mean(r.pipelines[-1]["kernel_ms"] for r in outs)
+    kern_ms = statistics.mean(r.kernel_ms for r in outs)
+    out = {
+        "workload": f"{WORKLOAD_NAME[query]} SF{sf:g}", "variant": cfg, "fact_rows": per,
+        "input_tuples": input_tuples, "value": input_tuples / (ms / 1e3), "unit": "tuples/s",
+        "fact_tuples_per_s": per / (ms / 1e3), "ms_per_step": ms, "kernels_ms": kern_ms,
+        "terminal_ms": term_ms, "steps": steps, "warmup": warmup,
+        "l2": "flushed between steps" if flush else "inputs larger than L2",
+        "roofline": {
+            "bound": "hbm", "peak": peak, "unit": "GB/s",
+            "terminal": {"bytes": acct["terminal"], "achieved": acct["terminal"] / term_ms / 1e6,
+                         "frac": acct["terminal"] / term_ms / 1e6 / peak},
+            "whole_query": {"bytes": acct["whole_query"], "achieved": acct["whole_query"] / ms / 1e6,
+                            "frac": acct["whole_query"] / ms / 1e6 / peak, "detail": acct["detail"]},
+            "traffic": ncu_traffic(query, sf),
+        },
+        "pipelines": [{k: p[k] for k in ("kernel_ms", "rows_in", "rows_out", "grid", "block")}
+                      for p in outs[-1].pipelines],
+    }
+    drop_tables(engine, query)
+    return out
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -327,7 +447,6 @@ def main():
         else:
             dist.init_process_group("gloo")
     from paper_1709_00700_b200 import Engine, _native
-    from paper_1709_00700_b200 import datagen as dg
     from paper_1709_00700_b200 import queries as Q
     from paper_1709_00700_b200.distributed import all_gather_rows
 
@@ -336,24 +455,14 @@ def main():
     cfg = args.config or DEFAULT_CONFIG[query]
     sql = Q.BENCH[query][0]
     engine = Engine(local)
-    engine.set_option("jit", args.jit)
-    engine.set_option("stage", args.stage)
-    if args.l2_distance is not None:
-        engine.set_option("l2_distance", args.l2_distance)
-    if args.pass_sync is not None:
-        engine.set_option("pass_sync", args.pass_sync)
-    if args.compact is not None:
-        engine.set_option("compact", args.compact)
-    if args.min_ctas is not None:
-        engine.set_option("min_ctas", args.min_ctas)
+    apply_options(engine, args)
     per_rank = load_tables(engine, query, sf, args.seed, rank, world)
     lib = _native.b200()
     stream = torch.cuda.ExternalStream(lib.hawk_b200_ctx_stream(engine.ctx), device=torch.device("cuda", local))
     l2 = torch.cuda.get_device_properties(local).L2_cache_size
-    dims = dims_for(query, sf * world)
-    alg_bytes = algorithmic_bytes(query, per_rank, dims)
-    flush = alg_bytes < 4 * l2
-
+    peak, peak_kind = measured_peak()
+    r0 = engine.run(sql, cfg) if world == 1 else None
+    acct = query_bytes(engine, query, sf, per_rank, world, r0, l2) if world == 1 else None
     xdev = torch.device("cuda", local) if args.backend == "nccl" else torch.device("cpu")
 
     def step():
@@ -367,27 +476,9 @@ def main():
         r = engine.finalize(sql, gathered, cfg)
         return r, part.launches + r.launches
 
-    for _ in range(args.warmup):
-        if flush:
-            engine.flush_l2()
-        r, _ = step()
-    kernel_ms, launches = [], 0
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    total_ms = 0.0
+    flush = (acct["whole_query"] if acct else per_rank * 8 * len(Q.FACT_COLUMNS[query])) < 4 * l2
     with Clocks(local) as clocks:
-        for _ in range(args.steps):
-            if flush:
-                engine.flush_l2()
-            start.record(stream)
-            r, n_launch = step()
-            end.record(stream)
-            end.synchronize()
-            total_ms += start.elapsed_time(end)
-            kernel_ms.append(r.kernel_ms if world == 1 else 0.0)
-            launches += n_launch
+        total_ms, outs = timed_steps(engine, stream, step, args.steps, args.warmup, flush, world=world)
         if world == 1:
             clocks.keep_busy(step)
         else:  # every rank runs the same number of extra (untimed) steps, ~0.4 s
@@ -395,63 +486,65 @@ def main():
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             for _ in range(min(20000, int(400.0 / max(float(t.item()), 1e-3)) + 1)):
                 step()
-    torch.cuda.synchronize()
     if world > 1:
         t = torch.tensor([total_ms], device=xdev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
     value = per_rank * world / (ms_per_step / 1e3)
+    launches = sum(n for _, n in outs)
 
-    # dominant kernel = the terminal pipeline's kernels (event-timed on the engine stream)
-    term = r.pipelines[-1] if r.pipelines else {"kernel_ms": 0.0}
-    peak, peak_kind = measured_peak()
-    term_ms = statistics.mean([p for p in kernel_ms]) if world == 1 else float("nan")
-    build_ms = sum(p["kernel_ms"] for p in r.pipelines[:-1]) if r.pipelines else 0.0
-    term_only_ms = max(1e-9, (term_ms - build_ms)) if world == 1 else float("nan")
-    fact_bytes = per_rank * len(Q.FACT_COLUMNS[query]) * 8
-    achieved = fact_bytes / (term_only_ms / 1e3) / 1e9 if world == 1 else None
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get(query)
-        except Exception:
-            traffic = None
     line = {
         "metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": f"{WORKLOAD_NAME[query]} SF{sf:g}" + (f" per GPU (x{world})" if world > 1 else ""),
-                   "query": query, "sf_per_gpu": sf, "fact_rows_per_gpu": per_rank, "variant": cfg,
-                   "l2": ("flushed between steps" if flush else
-                          f"inputs larger than L2 ({alg_bytes / 1e9:.2f} GB vs {l2 / 1e6:.0f} MB)"),
-                   "parallelism": f"dp{world} (fact rows sharded, dimensions replicated)"},
-        "hbm_gbs": alg_bytes / (ms_per_step / 1e3) / 1e9,
+        "vs_baseline": None, "dtype": "int64", "data": "synthetic (include/hawk_gen.h, generated in HBM)",
+        "config": workload_config(query, sf, world),
+        "variant": cfg,
+        "l2": ("flushed between steps" if flush else "inputs larger than L2 "
+               f"({per_rank * 8 * len(Q.FACT_COLUMNS[query]) / 1e9:.2f} GB vs {l2 / 1e6:.0f} MB)"),
         "gpu_launches": launches,
     }
     if world == 1:
-        line["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                            "frac": achieved / peak, "traffic": traffic,
-                            "kernel": "terminal pipeline (pipeline_kernel) of " + WORKLOAD_NAME[query],
-                            "algorithmic_bytes_per_launch": fact_bytes,
-                            "kernel_ms": term_only_ms, "peak_kind": peak_kind}
+        rs = [r for r, _ in outs]
+        term_ms = statistics.mean(r.pipelines[-1]["kernel_ms"] for r in rs)
+        achieved = acct["terminal"] / term_ms / 1e6
+        line["hbm_gbs"] = acct["whole_query"] / ms_per_step / 1e6
+        line["roofline"] = {
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": ncu_traffic(query, sf),
+            "kernel": f"terminal pipeline (hk_jit_pipeline) of {WORKLOAD_NAME[query]}",
+            "algorithmic_bytes_per_launch": acct["terminal"], "kernel_ms": term_ms,
+            "peak_kind": peak_kind,
+            "whole_query": {"bytes": acct["whole_query"], "achieved": line["hbm_gbs"],
+                            "frac": line["hbm_gbs"] / peak, "detail": acct["detail"]},
+        }
     line["clocks"] = clocks.summary()
 
     if not args.no_e2e:
         line["e2e"] = e2e_measure(engine, query, sf, args, step, rank, world, per_rank)
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
-        n_fact, times = cpu_reference_sample(query, sf, args.seed, args.cpu_sample_rows, reps=1)
-        ref_rate = n_fact / times[0]
-        threads = os.cpu_count() or 1
-        pn, pt = cpu_port(query, sf, args.seed, threads)
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from ref_sharded import ShardedReference
+        info = host_info()
+        sample = reference_sample_rows(query, sf, 1)
+        ref = ShardedReference(query, sf, args.seed, fact_rows=sample)
+        t = min(ref.timed(1))
         line["cpu_baseline"] = {
-            "value": ref_rate, "unit": "tuples/s", "cores": 1, "kind": "reference",
-            "sample": f"reference_execute (unmodified reference sources, oracle/_ref) over the first "
-                      f"{n_fact} fact rows of {WORKLOAD_NAME[query]} SF{sf:g}; single-threaded by design "
-                      f"(SPEC.md:179)"}
-        line["cpu_port"] = {"value": pn / pt, "unit": "tuples/s", "cores": threads, "kind": "port",
-                            "sample": f"oracle/port restatement over all {pn} fact rows, {threads} threads"}
+            "value": ref.fact_rows / t, "unit": "tuples/s", "cores": ref.threads, "kind": "reference",
+            "sample": f"reference_execute (unmodified reference sources, oracle/_ref) over {ref.fact_rows} "
+                      f"fact rows of {WORKLOAD_NAME[query]} SF{sf:g}, one row shard per host thread "
+                      f"({ref.shards} shards), merged; 1 run",
+            "cpu_model": info["cpu_model"], "host_cores": info["cores"]}
+        del ref
+    if world == 1 and not args.no_per_query and args.config is None and args.sf is None:
+        drop_tables(engine, query)
+        line["per_query"] = {}
+        for q in DEFAULT_CONFIG:
+            try:
+                line["per_query"][q] = measure_query(engine, stream, q, BASELINE_SF[q], DEFAULT_CONFIG[q],
+                                                     args.per_query_steps, 3, l2, peak)
+            except Exception as e:  # noqa: BLE001 - reported in the line
+                line["per_query"][q] = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     engine.close()
@@ -463,8 +556,8 @@ def e2e_measure(engine, query, sf, args, step, rank, world, per_rank):
     """Same metric through the engine's C ABI with HOST inputs: each step copies
     this rank's fact-table shard (the referenced columns) from pinned host
     memory into HBM (hawk_engine_put_columns), runs the query (N>1: partials,
-    NCCL all-gather, merge) and reads the result back (D2H). Timed per step as
-    the max over ranks."""
+    exchange, merge) and reads the result back (D2H). Timed per step as the max
+    over ranks."""
     import ctypes as C
 
     import numpy as np
@@ -512,7 +605,7 @@ def e2e_measure(engine, query, sf, args, step, rank, world, per_rank):
     return {"value": n * world / (ms / 1e3), "unit": "tuples/s", "h2d_bytes_per_step": h2d * world,
             "d2h_bytes_per_step": d2h, "ms_per_step": ms,
             "path": "hawk_engine_put_columns (pinned host -> HBM) + hawk_engine_run (C ABI)"
-                    + (" / run_partial + NCCL all-gather + finalize" if world > 1 else "")}
+                    + (" / run_partial + exchange + finalize" if world > 1 else "")}
 
 
 if __name__ == "__main__":

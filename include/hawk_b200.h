@@ -289,6 +289,8 @@ int32_t hawk_b200_free(hawk_ctx* ctx, void* d_ptr);
 int32_t hawk_b200_memcpy_h2d(hawk_ctx* ctx, void* d_dst, const void* src, size_t bytes);
 int32_t hawk_b200_memcpy_d2h(hawk_ctx* ctx, void* dst, const void* d_src, size_t bytes);
 int32_t hawk_b200_memset(hawk_ctx* ctx, void* d_ptr, int32_t value, size_t bytes);
+/* free and total HBM of the context's device (cudaMemGetInfo) */
+int32_t hawk_b200_mem_info(hawk_ctx* ctx, size_t* free_bytes, size_t* total_bytes);
 /* pinned host memory, for the end-to-end path */
 int32_t hawk_b200_host_alloc(size_t bytes, void** ptr);
 int32_t hawk_b200_host_free(void* ptr);

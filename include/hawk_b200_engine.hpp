@@ -84,6 +84,7 @@ struct DeviceTable {
   int64_t row_offset = 0;  // global row id of local row 0 (fact-table shards)
   std::vector<DeviceColumn> columns;
   TablePtr catalog;        // schema + lexicons for the front end
+  bool pooled = false;     // columns come from the engine's block pool (pair tables)
   int find(const std::string& column) const;
 };
 
@@ -205,6 +206,20 @@ std::vector<PipelineProgram> apply_variants(const PipelineSet& set,
                                             const std::vector<VariantConfiguration>& configs,
                                             std::vector<HashTableDescriptor>& descriptors,
                                             std::vector<VariantConfiguration>* effective = nullptr);
+
+/// CROSS_JOIN (planner_pipelines.cpp:337-352): a pair table of n_driver x
+/// n_aux rows in driver-major order that replaces LOOP(driver) + CROSS_JOIN(aux).
+struct CrossPairTable {
+  std::string name;        // catalog name (unique per rewrite)
+  int table = -1;          // its index in the rewritten PipelineSet::tables
+  int driver = -1, aux = -1;
+  int driver_columns = 0;  // pair columns [0, driver_columns) are the driver's
+  std::vector<bool> used;  // pair columns the terminal program reads
+};
+/// The plan half of the CROSS_JOIN lowering: appends a pair-table catalog per
+/// CROSS_JOIN of the terminal pipeline, reroutes CrossAux attributes to it and
+/// drops the op. Needs no device; the identity when there is no CROSS_JOIN.
+PipelineSet rewrite_cross_joins(const PipelineSet& set, std::vector<CrossPairTable>* pairs = nullptr);
 
 /// Lowers one (variant-applied) program into the POD device descriptor; the
 /// column slots are resolved against `tables` by the caller's binder.

@@ -52,6 +52,13 @@ int port_width(int query);
 int64_t port_run(int query, const int64_t* const* cols, int64_t n, const int64_t* dim_rows,
                  const int64_t* codes, int threads, int64_t* out, int64_t out_rows);
 
+/* The streaming form (SF100): the same query over fact rows
+ * [row_begin, row_begin + n) of the generated tables at scale factor sf, each
+ * worker regenerating its fact rows chunk by chunk (include/hawk_gen.h);
+ * dimension tables are generated whole. Nothing fact-sized is materialised. */
+int64_t port_run_gen(int query, double sf, uint64_t seed, int64_t row_begin, int64_t n,
+                     const int64_t* codes, int threads, int64_t* out, int64_t out_rows);
+
 #ifdef __cplusplus
 }
 #endif

@@ -392,15 +392,26 @@ bool valid_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
 // rows per thread per step so each warp writes 512 contiguous bytes
 __global__ void cross_expand_kernel(const int64_t* __restrict__ src, int64_t n_aux, int32_t side,
                                     int64_t n, int64_t padded, int64_t* __restrict__ out) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); i < padded; i += 2 * stride) {
+  const int64_t stride = 2 * (int64_t)gridDim.x * blockDim.x;
+  int64_t i = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  if (i >= padded) return;
+  // (driver, aux) of element i, stepped by the grid stride without a 64-bit
+  // division per element (one per thread up front)
+  const int64_t na = n_aux > 0 ? n_aux : 1;
+  int64_t q = i / na, r = i - q * na;
+  const int64_t dq = stride / na, dr = stride - dq * na;
+  for (; i < padded; i += stride) {
     int64_t v[2];
+    int64_t qq = q, rr = r;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      const int64_t r = i + k;
-      v[k] = r < n ? src[side == 0 ? r / n_aux : r % n_aux] : 0;
+      v[k] = i + k < n ? src[side == 0 ? qq : rr] : 0;
+      if (++rr == na) rr = 0, ++qq;
     }
     *reinterpret_cast<longlong2*>(out + i) = make_longlong2(v[0], v[1]);
+    q += dq;
+    r += dr;
+    if (r >= na) r -= na, ++q;
   }
 }
 
@@ -604,6 +615,12 @@ int32_t hawk_b200_memcpy_d2h(hawk_ctx* ctx, void* dst, const void* d_src, size_t
 }
 int32_t hawk_b200_memset(hawk_ctx* ctx, void* d_ptr, int32_t value, size_t bytes) {
   HK_TRY(cudaMemsetAsync(d_ptr, value, bytes, ctx->stream));
+  return HAWK_OK;
+}
+int32_t hawk_b200_mem_info(hawk_ctx* ctx, size_t* free_bytes, size_t* total_bytes) {
+  if (!ctx || !free_bytes || !total_bytes) return HAWK_ERR_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  HK_TRY(cudaMemGetInfo(free_bytes, total_bytes));
   return HAWK_OK;
 }
 int32_t hawk_b200_host_alloc(size_t bytes, void** ptr) {

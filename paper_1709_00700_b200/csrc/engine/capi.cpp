@@ -233,7 +233,7 @@ int32_t hawk_engine_finalize(hawk_engine* e, const char* sql, const char* config
                              const int64_t* const* data, const int64_t* rows, hawk_result** out) {
   *out = nullptr;
   return guard([&] {
-    const PipelineSet& set = cached_plan(e, sql);
+    const PipelineSet set = rewrite_cross_joins(cached_plan(e, sql));
     WorkloadConfig w = config && *config ? parse_workload_config(config) : WorkloadConfig();
     // widths come from the lowered terminal program
     const std::size_t T = static_cast<std::size_t>(set.terminal);
@@ -316,7 +316,7 @@ int32_t hawk_engine_space_config(hawk_engine* e, const char* sql, int32_t pipeli
 int32_t hawk_engine_validate(hawk_engine* e, const char* sql, const char* config, char* buf,
                              int32_t len) {
   return guard([&] {
-    PipelineSet set = plan_sql(e->engine, sql);
+    PipelineSet set = rewrite_cross_joins(plan_sql(e->engine, sql));
     auto configs = configs_for(set, config ? config : "");
     std::vector<HashTableDescriptor> desc;
     std::vector<PipelineProgram> progs = apply_variants(set, configs, desc);
@@ -333,7 +333,7 @@ int32_t hawk_engine_validate(hawk_engine* e, const char* sql, const char* config
 int32_t hawk_engine_compile_check(hawk_engine* e, const char* sql, const char* config, char* buf,
                                   int32_t len) {
   return guard([&] {
-    PipelineSet set = plan_sql(e->engine, sql);
+    PipelineSet set = rewrite_cross_joins(plan_sql(e->engine, sql));
     auto configs = configs_for(set, config ? config : "");
     std::vector<HashTableDescriptor> desc;
     std::vector<VariantConfiguration> eff;
@@ -380,7 +380,7 @@ int32_t hawk_engine_compile_check(hawk_engine* e, const char* sql, const char* c
 int32_t hawk_engine_explain(hawk_engine* e, const char* sql, const char* config, char* buf,
                             int32_t len) {
   return guard([&] {
-    PipelineSet set = plan_sql(e->engine, sql);
+    PipelineSet set = rewrite_cross_joins(plan_sql(e->engine, sql));
     auto configs = configs_for(set, config ? config : "");
     std::ostringstream os;
     for (std::size_t i = 0; i < set.pipelines.size(); ++i) {

@@ -4,7 +4,9 @@
 //
 // Replaces the reference's missing runtime_executor/engine
 // (proj/CMakeLists.txt:32-37); contract from SPEC.md:372-380.
+#include <atomic>
 #include <chrono>
+#include <limits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -147,8 +149,16 @@ struct Engine::Impl {
 
   void free_table(DeviceTable& t) {
     for (auto& c : t.columns)
-      if (c.d_data) hawk_b200_free(ctx, c.d_data);
+      if (c.d_data) {
+        if (t.pooled) release(c.d_data);
+        else hawk_b200_free(ctx, c.d_data);
+      }
     t.columns.clear();
+  }
+  size_t pooled_bytes() const {
+    size_t b = 0;
+    for (const auto& [sz, p] : pool) b += sz;
+    return b;
   }
 
   const DeviceTable& device_table(const PipelineSet& set, int table_id) const {
@@ -679,50 +689,51 @@ struct PhaseTrace {
 // CROSS_JOIN (planner_pipelines.cpp:337-352, oracle
 // planner_reference.cpp:188-203). The reference nests a loop over the
 // auxiliary table inside the driver loop; here the terminal pipeline's
-// LOOP(driver) ... CROSS_JOIN(aux) becomes LOOP over a device-materialised
-// pair table of n_driver x n_aux rows in driver-major order (one
-// hawk_b200_cross_expand per referenced column), so every op after it —
-// aux filters, probes keyed by aux columns, residual cross-table filters,
+// LOOP(driver) ... CROSS_JOIN(aux) becomes LOOP over a pair table of
+// n_driver x n_aux rows in driver-major order, so every op after it — aux
+// filters, probes keyed by aux columns, residual cross-table filters,
 // aggregation — runs unchanged on the fused kernel skeleton. Driver-side ops
 // before the CROSS_JOIN are evaluated once per pair, which is the same
-// result. Only the terminal pipeline can carry a CROSS_JOIN: build sides are
-// a scan (+select) of one table (sql_parser.cpp:607-611).
-struct CrossExpansion {
-  PipelineSet set;
-  std::vector<std::string> device_tables;  // pair tables to free after the run
-};
-
+// result. Only the terminal pipeline can carry a CROSS_JOIN: build sides are a
+// scan (+select) of one table (sql_parser.cpp:607-611).
+//
+// Two halves: rewrite_cross_joins is the plan rewrite (catalog only: used by
+// execute, finalize, explain and compile_check alike), materialise_cross
+// writes the referenced pair-table columns on the device.
 static bool has_cross_join(const PipelineProgram& p) {
   for (const PipelineOp& op : p.ops)
     if (op.kind == PipelineOpKind::CrossJoin) return true;
   return false;
 }
 
-static void expand_cross_joins(Engine::Impl& I, const PipelineSet& in, CrossExpansion& x) {
-  x.set = in;
+static std::atomic<int> g_cross_serial{0};
+
+PipelineSet rewrite_cross_joins(const PipelineSet& in, std::vector<CrossPairTable>* pairs) {
+  PipelineSet out = in;
+  if (in.terminal < 0 || static_cast<std::size_t>(in.terminal) >= in.pipelines.size()) return out;
   for (std::size_t i = 0; i < in.pipelines.size(); ++i)
     if (static_cast<int>(i) != in.terminal && has_cross_join(in.pipelines[i]))
       throw Unsupported("CROSS_JOIN outside the terminal pipeline");
-  PipelineProgram& prog = x.set.pipelines[static_cast<std::size_t>(in.terminal)];
-  static int serial = 0;
+  PipelineProgram& prog = out.pipelines[static_cast<std::size_t>(in.terminal)];
   for (;;) {
     std::size_t k = 0;
     while (k < prog.ops.size() && prog.ops[k].kind != PipelineOpKind::CrossJoin) ++k;
     if (k == prog.ops.size()) break;
     const int D = prog.driver_table, A = prog.ops[k].table;
-    const int X = static_cast<int>(x.set.tables.size());
-    const Table& dcat = *x.set.tables.at(static_cast<std::size_t>(D));
-    const Table& acat = *x.set.tables.at(static_cast<std::size_t>(A));
+    const int X = static_cast<int>(out.tables.size());
+    const Table& dcat = *out.tables.at(static_cast<std::size_t>(D));
+    const Table& acat = *out.tables.at(static_cast<std::size_t>(A));
     const int nd_cols = static_cast<int>(dcat.column_count());
     Schema schema;
     for (std::size_t c = 0; c < dcat.column_count(); ++c)
       schema.push_back({"d." + dcat.column_name(c), dcat.column(c).kind()});
     for (std::size_t c = 0; c < acat.column_count(); ++c)
       schema.push_back({"a." + acat.column_name(c), acat.column(c).kind()});
-    const std::string name = "__cross" + std::to_string(++serial) + ":" + dcat.name() + "*" + acat.name();
+    const std::string name =
+        "__cross" + std::to_string(++g_cross_serial) + ":" + dcat.name() + "*" + acat.name();
     auto cat = std::make_shared<Table>(name, schema);
     cat->finalize();
-    x.set.tables.push_back(cat);
+    out.tables.push_back(cat);
 
     // reroute: driver columns keep their index, aux columns follow them
     auto fix = [&](OpAttr& a) {
@@ -754,10 +765,16 @@ static void expand_cross_joins(Engine::Impl& I, const PipelineSet& in, CrossExpa
     prog.ops.front().table = X;
     prog.driver_table = X;
 
-    // materialise the referenced columns of the pair table
-    std::vector<bool> used(schema.size(), false);
+    // the pair-table columns the program reads
+    CrossPairTable pt;
+    pt.name = name;
+    pt.table = X;
+    pt.driver = D;
+    pt.aux = A;
+    pt.driver_columns = nd_cols;
+    pt.used.assign(schema.size(), false);
     auto mark = [&](const OpAttr& a) {
-      if (a.route == AttrRoute::Driver && a.table == X) used.at(static_cast<std::size_t>(a.column)) = true;
+      if (a.route == AttrRoute::Driver && a.table == X) pt.used.at(static_cast<std::size_t>(a.column)) = true;
     };
     for (const PipelineOp& op : prog.ops) {
       for (const OpComparison& c : op.predicate) {
@@ -772,32 +789,53 @@ static void expand_cross_joins(Engine::Impl& I, const PipelineSet& in, CrossExpa
       for (const OpAggregate& g : op.aggregates)
         if (g.input.kind == OpOperand::Kind::Attr) mark(g.input.attr);
     }
-    const DeviceTable& dd = I.device_table(x.set, D);
-    const DeviceTable& ad = I.device_table(x.set, A);
-    DeviceTable dt;
-    dt.name = name;
-    dt.rows = dd.rows * ad.rows;
-    dt.catalog = cat;
-    const size_t bytes = static_cast<size_t>(padded_rows(dt.rows)) * 8;
-    x.device_tables.push_back(name);
-    I.tables[name] = DeviceTable{name, 0, 0, {}, cat};  // freed by the caller even on error
-    for (std::size_t c = 0; c < schema.size(); ++c) {
-      if (!used[c]) continue;
-      const bool aux = static_cast<int>(c) >= nd_cols;
-      const int src_col = aux ? static_cast<int>(c) - nd_cols : static_cast<int>(c);
-      const DeviceColumn& src = I.device_column(x.set, aux ? A : D, src_col);
+    if (pairs) pairs->push_back(std::move(pt));
+  }
+  return out;
+}
+
+// Writes the referenced columns of every pair table (registered in the
+// device store under its catalog name; the caller drops them after the run).
+static void materialise_cross(Engine::Impl& I, const PipelineSet& set,
+                              const std::vector<CrossPairTable>& pairs,
+                              std::vector<std::string>& registered) {
+  for (const CrossPairTable& pt : pairs) {
+    const DeviceTable& dd = I.device_table(set, pt.driver);
+    const DeviceTable& ad = I.device_table(set, pt.aux);
+    // size guard: the pair count and every column's bytes must fit int64 and HBM
+    if (dd.rows > 0 && ad.rows > std::numeric_limits<int64_t>::max() / 8 / dd.rows)
+      throw CapacityExceeded("CROSS_JOIN of " + dd.name + " x " + ad.name + " overflows the pair count");
+    const int64_t rows = dd.rows * ad.rows;
+    const size_t bytes = static_cast<size_t>(padded_rows(rows)) * 8;
+    size_t ncols = 0;
+    for (bool u : pt.used) ncols += u ? 1 : 0;
+    size_t free_b = 0, total_b = 0;
+    if (hawk_b200_mem_info(I.ctx, &free_b, &total_b) == HAWK_OK && ncols > 0 &&
+        bytes > (free_b + I.pooled_bytes()) / ncols)
+      throw CapacityExceeded("CROSS_JOIN of " + dd.name + " (" + std::to_string(dd.rows) + " rows) x " +
+                             ad.name + " (" + std::to_string(ad.rows) + " rows) needs " +
+                             std::to_string(ncols) + " pair columns of " + std::to_string(bytes) +
+                             " bytes; " + std::to_string(free_b) + " bytes of HBM are free");
+    registered.push_back(pt.name);
+    DeviceTable& dt = I.tables[pt.name];
+    dt = DeviceTable{pt.name, 0, 0, {}, set.tables.at(static_cast<std::size_t>(pt.table))};
+    dt.pooled = true;
+    const Table& cat = *dt.catalog;
+    for (std::size_t c = 0; c < pt.used.size(); ++c) {
+      if (!pt.used[c]) continue;
+      const bool aux = static_cast<int>(c) >= pt.driver_columns;
+      const int src_col = aux ? static_cast<int>(c) - pt.driver_columns : static_cast<int>(c);
+      const DeviceColumn& src = I.device_column(set, aux ? pt.aux : pt.driver, src_col);
       DeviceColumn col;
-      col.name = schema[c].name;
+      col.name = cat.column_name(c);
       col.kind = src.kind;
       col.distinct = src.distinct;
-      void* p = nullptr;
-      check(hawk_b200_alloc(I.ctx, bytes, &p), "cross-join column allocation");
-      col.d_data = static_cast<int64_t*>(p);
-      I.tables[name].columns.push_back(col);
+      col.d_data = static_cast<int64_t*>(I.acquire(bytes));
+      dt.columns.push_back(col);
       check(hawk_b200_cross_expand(I.ctx, src.d_data, dd.rows, ad.rows, aux ? 1 : 0, col.d_data),
             "cross-join expansion");
     }
-    I.tables[name].rows = dt.rows;
+    dt.rows = rows;
   }
 }
 
@@ -807,9 +845,11 @@ static QueryRun run_query(Engine& e, Engine::Impl& I, const PipelineSet& set,
   if (set.terminal >= 0 && static_cast<std::size_t>(set.terminal) < set.pipelines.size() &&
       has_cross_join(set.pipelines[static_cast<std::size_t>(set.terminal)])) {
     require_device(e.ctx());
-    CrossExpansion x;
+    std::vector<CrossPairTable> pairs;
+    const PipelineSet x = rewrite_cross_joins(set, &pairs);
+    std::vector<std::string> registered;
     auto cleanup = [&]() {
-      for (const std::string& n : x.device_tables) {
+      for (const std::string& n : registered) {
         auto it = I.tables.find(n);
         if (it == I.tables.end()) continue;
         I.free_table(it->second);
@@ -817,8 +857,8 @@ static QueryRun run_query(Engine& e, Engine::Impl& I, const PipelineSet& set,
       }
     };
     try {
-      expand_cross_joins(I, set, x);
-      QueryRun r = run_query(e, I, x.set, configs, m, partial);
+      materialise_cross(I, x, pairs, registered);
+      QueryRun r = run_query(e, I, x, configs, m, partial);
       cleanup();
       return r;
     } catch (...) {
@@ -1069,9 +1109,10 @@ Table Engine::finalize_partials(const PipelineSet& set, const WorkloadConfig& co
   return finalize_partials_columns(set, config, parts).to_table();
 }
 
-ResultColumns Engine::finalize_partials_columns(const PipelineSet& set, const WorkloadConfig& config,
+ResultColumns Engine::finalize_partials_columns(const PipelineSet& set_in, const WorkloadConfig& config,
                                                 const std::vector<PartialResult>& parts) {
   require_device(ctx_);
+  const PipelineSet set = rewrite_cross_joins(set_in);
   auto configs = per_pipeline(set, config);
   const std::size_t T = static_cast<std::size_t>(set.terminal);
   PipelineProgram terminal = apply_variant(set.pipelines[T], configs[T]);

@@ -64,6 +64,7 @@ def port():
         _sig(lib, "port_width", i32, i32)
         _sig(lib, "port_run", i64, i32, C.POINTER(vp), i64, C.POINTER(i64), C.POINTER(i64), i32,
              vp, i64)
+        _sig(lib, "port_run_gen", i64, i32, f64, u64, i64, i64, C.POINTER(i64), i32, vp, i64)
         _port = lib
     return _port
 
@@ -197,6 +198,34 @@ class OraDb:
 def result_table(result) -> OraTable:
     """Engine Result -> reference Table for compare_result_tables."""
     return OraTable.from_columns("result", result.columns)
+
+
+def port_gen(table: int, col: int, sf: float, seed: int, begin: int, n: int,
+             threads: int = 0) -> np.ndarray:
+    """Rows [begin, begin + n) of a generated column (include/hawk_gen.h) on
+    the host, without the product library."""
+    out = np.empty(max(n, 0), dtype=np.int64)
+    if n > 0:
+        port().port_gen(table, col, sf, seed, begin, n, out.ctypes.data, threads or (os.cpu_count() or 1))
+    return out
+
+
+def port_run_gen(query: int, sf: float, seed: int, codes: list[int], threads: int,
+                 out_rows: int, row_begin: int = 0, n: int | None = None) -> np.ndarray:
+    """The streaming restatement (oracle/port, port_run_gen): fact rows are
+    regenerated chunk by chunk per worker, so SF100 needs no host table."""
+    from paper_1709_00700_b200 import datagen as dg
+    lib = port()
+    fact = dg.LINEORDER if query in (2, 3) else dg.LINEITEM
+    if n is None:
+        n = dg.table_rows(fact, sf) - row_begin
+    cds = (i64 * max(1, len(codes)))(*codes)
+    w = lib.port_width(query)
+    out = np.zeros((max(1, out_rows), w), dtype=np.int64)
+    r = lib.port_run_gen(query, sf, seed, row_begin, n, cds, threads, out.ctypes.data, out_rows)
+    if r < 0:
+        raise RuntimeError("port output buffer too small")
+    return out[:r]
 
 
 def port_run(query: int, cols: list[np.ndarray], n: int, dim_rows: list[int], codes: list[int],

@@ -94,9 +94,13 @@ def _port_inputs(key, sf, seed):
     raise KeyError(key)
 
 
-def port_rows(key, sf, seed, threads=4):
-    q, cols, n, dims, codes = _port_inputs(key, sf, seed)
-    out = port_run(q, cols, n, dims, codes, threads, out_rows=max(1024, n))
+PORT_QUERY = {"tpch_q6": 0, "tpch_q1": 1, "ssb_q11": 2, "ssb_q41": 3, "tpch_q3": 4}
+# generator codes of the string literals each query compares with (hawk_gen.h
+# lexicons): 'AMERICA' = 1 (c_region, s_region), 'MFGR#3..5' = 2, 3, 4; 'BUILDING' = 1
+PORT_CODES = {"tpch_q6": [], "tpch_q1": [], "ssb_q11": [], "ssb_q41": [1, 1, 2, 3, 4], "tpch_q3": [1]}
+
+
+def _port_decode(key, out):
     rows = []
     for r in out:
         vals = [int(v) for v in r]
@@ -106,6 +110,18 @@ def port_rows(key, sf, seed, threads=4):
     return sorted(rows)
 
 
+def port_rows(key, sf, seed, threads=4):
+    """The streaming restatement over the generated tables (any SF)."""
+    from oracle_bridge import port_run_gen
+    cap = dg.table_rows(dg.ORDERS, sf) if key == "tpch_q3" else 1024
+    return _port_decode(key, port_run_gen(PORT_QUERY[key], sf, seed, PORT_CODES[key], threads, cap))
+
+
+def port_rows_materialised(key, sf, seed, threads=4):
+    q, cols, n, dims, codes = _port_inputs(key, sf, seed)
+    return _port_decode(key, port_run(q, cols, n, dims, codes, threads, out_rows=max(1024, n)))
+
+
 @pytest.mark.parametrize("key", [k for k, _ in harness.BENCH])
 @pytest.mark.parametrize("sf", [0.01, 0.05])
 def test_port_matches_reference_execute(key, sf):
@@ -113,6 +129,7 @@ def test_port_matches_reference_execute(key, sf):
     db = harness.oracle_db(harness.bench_tables(db_name, sf, 42))
     ref = db.execute(dict(harness.BENCH)[key]).canonical_rows()
     ours = port_rows(key, sf, 42)
+    assert ours == port_rows_materialised(key, sf, 42)
     assert len(ref) == len(ours)
     for a, b in zip(ref, ours):
         for x, y in zip(a, b):
@@ -141,10 +158,9 @@ def test_cross_join_oracle_closed_form():
                                         Column("a_w", INT64, a_w)]))
     lo = {c.name: np.asarray(c.values) for c in tables[0].columns()}
     q = lo["lo_quantity"]
-    res = db.execute("select count(*), sum(lo_quantity*a_w) from xa, lineorder "
+    res = db.execute("select count(*) as n, sum(lo_quantity*a_w) as s from xa, lineorder "
                      "where a_w < 5 and lo_quantity < 10")
-    cols = {c.name: np.asarray(c.values) for c in res.columns()}
-    vals = sorted(int(v[0]) for v in cols.values())
-    want = sorted([int((q < 10).sum()) * int((a_w < 5).sum()),
-                   int(q[q < 10].sum()) * int(a_w[a_w < 5].sum())])
-    assert vals == want
+    cols = res.columns()
+    assert [c.name for c in cols] == ["n", "s"]
+    assert int(cols[0].values[0]) == int((q < 10).sum()) * int((a_w < 5).sum())
+    assert int(cols[1].values[0]) == int(q[q < 10].sum()) * int(a_w[a_w < 5].sum())

@@ -98,10 +98,15 @@ def test_lowering_q3_payload_chain(tpch):
     assert text.count("SINK HASH_PUT") == 2 and "SINK HASH_AGGREGATE" in text
 
 
-def test_cross_join_is_reported_unsupported(micro):
+def test_cross_join_lowers_to_pair_table(micro):
+    # CROSS_JOIN (planner_pipelines.cpp:337-352) is rewritten into a LOOP over
+    # a pair table (engine.cpp rewrite_cross_joins) for explain, compile_check
+    # and finalize as for execution
     sql = "select lo_quantity, p_size from part, lineorder where p_size < 2 and lo_quantity < 2"
-    with pytest.raises(Unsupported):
-        micro.explain(sql, f"{PROJ};{AGG}")
+    text = micro.explain(sql, f"{PROJ};{AGG}")
+    assert "__cross" in text and "lineorder*part" in text
+    report = micro.compile_check(sql, f"{PROJ};{AGG}")
+    assert all(" ok " in l for l in report.splitlines() if l), report
 
 
 @pytest.mark.parametrize("key", [k for k, _ in harness.BENCH])
