@@ -219,7 +219,8 @@ def workload_config(query: str, sf: float, world: int) -> dict:
     cfg = {"workload": f"{WORKLOAD_NAME[query]} SF{sf * world:g}", "query": query, "sf": sf * world,
            "fact_rows": per * world}
     if world > 1:
-        cfg["parallelism"] = f"dp{world} (fact rows sharded, SF{sf:g} per GPU)"
+        cfg["parallelism"] = (f"dp{world} (fact rows sharded, SF{sf:g} per GPU"
+                              + (", orders co-partitioned by orderkey)" if query == "tpch_q3" else ")"))
     return cfg
 
 
@@ -336,15 +337,21 @@ def run_reference_arm(args):
 
 def load_tables(engine, query: str, sf: float, seed: int, rank: int, world: int):
     """Generates the query's tables in HBM: the fact table as this rank's shard
-    of an (world x sf) table, dimensions replicated."""
+    of an (world x sf) table, dimensions replicated — except TPC-H orders,
+    which is co-partitioned with lineitem by orderkey range
+    (distributed.copartition_range), so Q3's orders build scales as 1/N."""
     from paper_1709_00700_b200 import datagen as dg
     from paper_1709_00700_b200 import queries as Q
+    from paper_1709_00700_b200.distributed import copartition_range
     _, tables, fact = Q.BENCH[query]
     global_sf = sf * world
     per = dg.table_rows(fact, sf)
     for t in tables:
         if t == fact:
             engine.generate(t, global_sf, seed, rank * per, per)
+        elif fact == dg.LINEITEM and t == dg.ORDERS and world > 1:
+            b, e = copartition_range(rank * per, (rank + 1) * per)
+            engine.generate(t, global_sf, seed, b, e - b)
         else:
             engine.generate(t, global_sf, seed)
     return per
@@ -359,9 +366,20 @@ def drop_tables(engine, query: str):
             engine.drop(name)
 
 
+class StepInfo:
+    """What a timed step keeps of its result: the metrics only (holding every
+    Result alive would make each step allocate fresh host pages)."""
+
+    def __init__(self, r, launches=None):
+        self.kernel_ms = r.kernel_ms
+        self.pipelines = r.pipelines
+        self.launches = r.launches if launches is None else launches
+        self.rows = r.rows
+
+
 def timed_steps(engine, stream, step, steps, warmup, flush, clocks=None, world=1):
     """W untimed steps, then K steps each bracketed by CUDA events on the
-    engine's stream. Returns (total ms, per-step results)."""
+    engine's stream. Returns (total ms, per-step StepInfo)."""
     import torch
     for _ in range(warmup):
         if flush:
@@ -376,8 +394,10 @@ def timed_steps(engine, stream, step, steps, warmup, flush, clocks=None, world=1
         if flush:
             engine.flush_l2()
         start.record(stream)
-        outs.append(step())
+        r = step()
         end.record(stream)
+        outs.append(StepInfo(*r) if isinstance(r, tuple) else StepInfo(r))
+        del r
         end.synchronize()
         total_ms += start.elapsed_time(end)
     torch.cuda.synchronize()
@@ -464,12 +484,27 @@ def main():
     r0 = engine.run(sql, cfg) if world == 1 else None
     acct = query_bytes(engine, query, sf, per_rank, world, r0, l2) if world == 1 else None
     xdev = torch.device("cuda", local) if args.backend == "nccl" else torch.device("cpu")
+    comm = None
+    if world > 1 and args.backend == "nccl":
+        # the engine's own NCCL communicator (include/hawk_b200_comm.h); torch
+        # only ships its 128-byte id from rank 0
+        from paper_1709_00700_b200 import Communicator
+        uid = torch.zeros(128, dtype=torch.uint8, device=xdev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(Communicator.unique_id()), dtype=torch.uint8))
+        torch.distributed.broadcast(uid, 0)
+        comm = Communicator(engine, world, rank, bytes(uid.cpu().numpy().tobytes()))
 
     def step():
-        """One query: (result, kernels launched). N>1: shard partials, NCCL
-        all-gather of the partial rows, device merge + finalise."""
+        """One query: (result, kernels launched). N>1: every rank runs its
+        shard, the partials stay in HBM and are gathered to rank 0 with NCCL
+        over device buffers, merged there on the device (Engine.run_sharded).
+        --backend gloo (ranks sharing one GPU): host exchange + finalize."""
         if world == 1:
             r = engine.run(sql, cfg)
+            return r, r.launches
+        if comm is not None:
+            r = engine.run_sharded(sql, cfg, comm)
             return r, r.launches
         part = engine.run_partial(sql, cfg)
         gathered = all_gather_rows(part.rows, device=xdev)
@@ -492,7 +527,7 @@ def main():
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
     value = per_rank * world / (ms_per_step / 1e3)
-    launches = sum(n for _, n in outs)
+    launches = sum(o.launches for o in outs)
 
     line = {
         "metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": world, "steps": args.steps,
@@ -505,8 +540,7 @@ def main():
         "gpu_launches": launches,
     }
     if world == 1:
-        rs = [r for r, _ in outs]
-        term_ms = statistics.mean(r.pipelines[-1]["kernel_ms"] for r in rs)
+        term_ms = statistics.mean(o.pipelines[-1]["kernel_ms"] for o in outs)
         achieved = acct["terminal"] / term_ms / 1e6
         line["hbm_gbs"] = acct["whole_query"] / ms_per_step / 1e6
         line["roofline"] = {
@@ -547,6 +581,8 @@ def main():
                 line["per_query"][q] = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     engine.close()
     if world > 1:
         torch.distributed.destroy_process_group()

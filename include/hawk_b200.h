@@ -171,6 +171,14 @@ typedef struct hawk_table {
   uint64_t* d_bits;
   int64_t bits_lo;
   int64_t bits_span;
+  /* join tables over a dense key range (the engine's "dense_join" option):
+   * a direct-addressed index, d_index[key - index_lo] = build row id or -1 for
+   * key - index_lo in [0, index_span). When set it replaces the slots: builds
+   * CAS the key's entry (a second claim is a DuplicateKey), probes read one
+   * 4-byte entry. NULL = the LP / cuckoo slots above are the table. */
+  int32_t* d_index;
+  int64_t index_lo;
+  int64_t index_span;
 } hawk_table;
 
 /* A lowered pipeline program: LOOP over the driver, FILTER conjuncts on the
@@ -258,6 +266,8 @@ int32_t hawk_b200_device_count(int32_t* count);
 int32_t hawk_b200_ctx_create(int32_t device, hawk_ctx** out);
 int32_t hawk_b200_ctx_destroy(hawk_ctx* ctx);
 int32_t hawk_b200_ctx_sm_count(hawk_ctx* ctx, int32_t* sms);
+/* CUDA device ordinal of the context */
+int32_t hawk_b200_ctx_device(hawk_ctx* ctx);
 /* cudaStream_t of the context, as void* */
 void* hawk_b200_ctx_stream(hawk_ctx* ctx);
 int32_t hawk_b200_ctx_synchronize(hawk_ctx* ctx);
@@ -272,6 +282,9 @@ int32_t hawk_b200_ctx_synchronize(hawk_ctx* ctx);
  * "min_ctas" (compiled: __launch_bounds__ minimum CTAs per SM; 0 = by unroll),
  * "priv_groups" (HASH_AGGREGATE local: groups with thread-private accumulators). */
 int32_t hawk_b200_ctx_set_option(hawk_ctx* ctx, const char* name, int64_t value);
+/* Reads an option back ("dense_join": 1 = join builds over a dense key range
+ * use a direct-addressed index instead of the variant's hash table; default 1). */
+int32_t hawk_b200_ctx_get_option(hawk_ctx* ctx, const char* name, int64_t* value);
 
 /* ---- compiled programs (the paper's code generation, §7) --------- */
 /* The CUDA source generated for a lowered pipeline under a variant: the
@@ -289,6 +302,8 @@ int32_t hawk_b200_free(hawk_ctx* ctx, void* d_ptr);
 int32_t hawk_b200_memcpy_h2d(hawk_ctx* ctx, void* d_dst, const void* src, size_t bytes);
 int32_t hawk_b200_memcpy_d2h(hawk_ctx* ctx, void* dst, const void* d_src, size_t bytes);
 int32_t hawk_b200_memset(hawk_ctx* ctx, void* d_ptr, int32_t value, size_t bytes);
+/* asynchronous device-to-device copy on the context stream */
+int32_t hawk_b200_memcpy_d2d(hawk_ctx* ctx, void* d_dst, const void* d_src, size_t bytes);
 /* free and total HBM of the context's device (cudaMemGetInfo) */
 int32_t hawk_b200_mem_info(hawk_ctx* ctx, size_t* free_bytes, size_t* total_bytes);
 /* pinned host memory, for the end-to-end path */
@@ -346,6 +361,17 @@ int32_t hawk_b200_exclusive_prefix_sum(hawk_ctx* ctx, const int64_t* d_flags, in
 int32_t hawk_b200_run_pipeline(hawk_ctx* ctx, const hawk_pipeline* pipeline,
                                const hawk_variant* variant, hawk_output* out,
                                hawk_metrics* metrics);
+/* hawk_b200_run_pipeline plus, for HASH_AGGREGATE, the group compaction of
+ * hawk_b200_agg_table_extract queued right behind the pipeline: out->rows is
+ * the number of groups, out->d_values the compacted (keys..., accs...) rows,
+ * and when out->rows <= h_cap_rows they were also copied into the (pinned)
+ * host buffer h_rows (out->h_values = h_rows) with the same single
+ * synchronisation; otherwise out->h_values is NULL. Other sinks: as
+ * hawk_b200_run_pipeline. */
+int32_t hawk_b200_run_pipeline_extract(hawk_ctx* ctx, const hawk_pipeline* pipeline,
+                                       const hawk_variant* variant, int64_t* h_rows,
+                                       int64_t h_cap_rows, hawk_output* out,
+                                       hawk_metrics* metrics);
 /* Layout-only twin of hawk_b200_agg_table_create (caller allocates). */
 int32_t hawk_b200_agg_table_layout(const hawk_pipeline* pipeline, int32_t impl, int32_t function,
                                    uint64_t seed, int64_t groups_bound, hawk_table* out,
@@ -365,6 +391,10 @@ int32_t hawk_b200_agg_table_extract(hawk_ctx* ctx, const hawk_pipeline* pipeline
  * (multi-GPU merge after an all-gather). */
 int32_t hawk_b200_agg_table_merge_rows(hawk_ctx* ctx, const hawk_pipeline* pipeline,
                                        hawk_table* table, const int64_t* d_rows, int64_t nrows);
+/* Combines n partial AGGREGATE rows (pipeline.naggs accumulators each) into
+ * one row at d_out (multi-GPU merge of non-grouped aggregates; asynchronous). */
+int32_t hawk_b200_agg_rows_combine(hawk_ctx* ctx, const hawk_pipeline* pipeline,
+                                   const int64_t* d_rows, int64_t n, int64_t* d_out);
 #endif /* !__CUDACC_RTC__ */
 
 #ifdef __cplusplus

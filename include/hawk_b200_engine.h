@@ -57,6 +57,13 @@ int32_t hawk_engine_run(hawk_engine* e, const char* sql, const char* config, haw
 /* shard execution: partial aggregates / projections before the cross-GPU merge */
 int32_t hawk_engine_run_partial(hawk_engine* e, const char* sql, const char* config,
                                 hawk_partial** out);
+/* multi-GPU: this rank's shard, NCCL gather of the partials to `root`, device
+ * merge there (hawk::b200::Engine::execute_sharded); comm from
+ * hawk_nccl_comm_create (include/hawk_b200_comm.h). Non-root ranks get an
+ * empty result with the query's columns. */
+struct hawk_comm;
+int32_t hawk_engine_run_sharded(hawk_engine* e, const char* sql, const char* config,
+                                struct hawk_comm* comm, int32_t root, hawk_result** out);
 int64_t hawk_partial_rows(const hawk_partial* p);
 int32_t hawk_partial_width(const hawk_partial* p);
 int32_t hawk_partial_sink(const hawk_partial* p);

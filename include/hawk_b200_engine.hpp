@@ -34,6 +34,7 @@
 #include "hawk/planner/pipelines.hpp"
 #include "hawk/storage/table.hpp"
 #include "hawk_b200.h"
+#include "hawk_b200_comm.h"
 
 namespace hawk::b200 {
 
@@ -184,6 +185,13 @@ class Engine {
                           const std::vector<PartialResult>& parts);
   ResultColumns finalize_partials_columns(const PipelineSet& set, const WorkloadConfig& config,
                                           const std::vector<PartialResult>& parts);
+  /// Multi-GPU execution over a fact-table shard per rank: runs the query on
+  /// this rank's shard, gathers every rank's partial result to `root` with
+  /// NCCL over device buffers (include/hawk_b200_comm.h) and merges it on the
+  /// root's device. The root returns the query result; the other ranks an
+  /// empty one (same columns, no rows).
+  ResultColumns execute_sharded(const PipelineSet& set, const WorkloadConfig& config, hawk_comm* comm,
+                                int root = 0, ExecutionMetrics* metrics = nullptr);
   /// Bumped by every change to the device store (plan caches key on it).
   uint64_t catalog_generation() const { return generation_; }
 

@@ -83,6 +83,23 @@ def b200() -> C.CDLL:
         _sig(lib, "hawk_b200_agg_table_reset", i32, vp, vp, vp)
         _sig(lib, "hawk_b200_agg_table_extract", i32, vp, vp, vp, vp)
         _sig(lib, "hawk_b200_agg_table_merge_rows", i32, vp, vp, vp, vp, i64)
+        _sig(lib, "hawk_b200_agg_rows_combine", i32, vp, vp, vp, i64, vp)
+        _sig(lib, "hawk_b200_memcpy_d2d", i32, vp, vp, vp, C.c_size_t)
+        _sig(lib, "hawk_b200_mem_info", i32, vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t))
+        _sig(lib, "hawk_b200_ctx_get_option", i32, vp, cp, C.POINTER(i64))
+        _sig(lib, "hawk_b200_ctx_device", i32, vp)
+        # include/hawk_b200_comm.h
+        _sig(lib, "hawk_nccl_available", i32)
+        _sig(lib, "hawk_nccl_unique_id", i32, vp)
+        _sig(lib, "hawk_nccl_comm_create", i32, vp, i32, i32, vp, C.POINTER(vp))
+        _sig(lib, "hawk_nccl_comm_destroy", i32, vp)
+        _sig(lib, "hawk_nccl_comm_rank", i32, vp)
+        _sig(lib, "hawk_nccl_comm_size", i32, vp)
+        _sig(lib, "hawk_nccl_allreduce", i32, vp, vp, vp, C.c_size_t, i32, i32)
+        _sig(lib, "hawk_nccl_allgather", i32, vp, vp, vp, C.c_size_t)
+        _sig(lib, "hawk_nccl_bcast", i32, vp, vp, C.c_size_t, i32)
+        _sig(lib, "hawk_nccl_alltoall", i32, vp, vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t), vp,
+             C.POINTER(C.c_size_t), C.POINTER(C.c_size_t))
         _b200 = lib
     return _b200
 
@@ -108,6 +125,7 @@ def engine() -> C.CDLL:
         _sig(lib, "hawk_engine_flush_l2", i32, vp)
         _sig(lib, "hawk_engine_run", i32, vp, cp, cp, C.POINTER(vp))
         _sig(lib, "hawk_engine_run_partial", i32, vp, cp, cp, C.POINTER(vp))
+        _sig(lib, "hawk_engine_run_sharded", i32, vp, cp, cp, vp, i32, C.POINTER(vp))
         _sig(lib, "hawk_partial_rows", i64, vp)
         _sig(lib, "hawk_partial_width", i32, vp)
         _sig(lib, "hawk_partial_sink", i32, vp)

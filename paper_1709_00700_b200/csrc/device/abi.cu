@@ -31,8 +31,11 @@ struct hawk_ctx {
   int dense_keys = 1;       // HAGG_LOCAL compiled: dense key-index lookaside when provided
   int compact = 1;          // compiled, branched: compact live rows after the first probe
   int min_ctas = 0;         // compiled: __launch_bounds__ min CTAs/SM override (0 = default)
-  int priv_groups = 64;     // HAGG_LOCAL: groups with thread-private accumulators
-  int jit = 0;              // compiled programs (jit.cu) instead of the interpreter
+  int priv_groups = -1;     // HAGG_LOCAL: groups with thread-private accumulators (-1 = auto)
+  int jit = 1;              // compiled programs (jit.cu) instead of the interpreter
+  int dense_join = 1;       // engine: dense-key join builds use a direct-addressed index
+  int drain_rows = 0;       // compiled, compacted: queued rows per lane per drain (0 = auto)
+  int split_bits = 1;       // compiled, compacted: key bitmaps for the first (1) / every (2) probe
   // COALESCED: stage pass tiles in smem with TMA. Off by default since the
   // private-accumulator group-by: TPC-H Q1 SF10 terminal 0.744 -> 0.712 ms
   // unstaged without the pass barrier, TPC-H Q6 unchanged (0.0343 ms both;
@@ -235,10 +238,14 @@ bool layout_smem(hawk_ctx* ctx, hk::KParams& kp, int role, int access, int impl,
   kp.priv_groups = 0;
   kp.smem_dense_off = 0;
   kp.smem_ord_off = kp.smem_priv_off = (int)off;
-  if (role == hk::K_HAGG_LOCAL && p.naggs > 0 && ctx->priv_groups > 0) {
+  // thread-private accumulators pay off when nearly every row updates a group
+  // (scan + group-by, TPC-H Q1); after probes the update rate is low and the
+  // CTA table's shared-memory atomics suffice (auto: -1)
+  const int priv_limit = ctx->priv_groups >= 0 ? ctx->priv_groups : (p.nprobe == 0 ? 64 : 0);
+  if (role == hk::K_HAGG_LOCAL && p.naggs > 0 && priv_limit > 0) {
     // thread-private accumulators for the first GP groups of each CTA
     const size_t per_group = (size_t)p.naggs * block * 8;
-    int gp = (int)std::min<size_t>((size_t)ctx->priv_groups, (48 * 1024) / per_group);
+    int gp = (int)std::min<size_t>((size_t)priv_limit, (48 * 1024) / per_group);
     const int local_slots = (1 << kp.local_log2) * (impl == HAWK_CUCKOO ? 2 : 1);
     const size_t need = ((off + 127) & ~size_t(127)) + (size_t)(local_slots + gp + 1) * 4 + 128 +
                         (size_t)gp * per_group;
@@ -258,11 +265,18 @@ bool layout_smem(hawk_ctx* ctx, hk::KParams& kp, int role, int access, int impl,
       }
     }
   }
+  if (role == hk::K_HAGG_LOCAL && kp.priv_groups == 0 && kp_jit && ctx->dense_keys &&
+      p.dense_groups > 0 && p.dense_groups <= 4096) {
+    // dense key index -> CTA table slot (the lookaside without private accumulators)
+    off = (off + 127) & ~size_t(127);
+    kp.smem_dense_off = (int)off;
+    off += (size_t)p.dense_groups * 4;
+  }
   kp.smem_queue_off = 0;
-  if (kp_jit && kp.split) {  // per-warp queues of compacted rows: 32 * R entries of 8 B
+  if (kp_jit && kp.split) {  // per-warp queues of compacted rows: 32 * (R + D) entries of 8 B
     off = (off + 127) & ~size_t(127);
     kp.smem_queue_off = (int)off;
-    off += (size_t)((block + 31) / 32) * 32 * R * 8;
+    off += (size_t)((block + 31) / 32) * 32 * (R + std::max(1, kp.split_drain)) * 8;
   }
   if (off > (size_t)ctx->smem_optin) return false;
   *smem_out = off;
@@ -302,6 +316,16 @@ int32_t occupancy(int role, const hawk_variant& v, int block, size_t smem, int* 
 // compiled, branched programs with a probe compact their live rows after it
 // (worth it when work follows the first probe: more probes or a group-by;
 // SSB Q1.1's single probe + SUM gains nothing)
+// queued rows per lane per drain when the context leaves it to the program:
+// batching pays off for probe chains (SSB Q4.1: 3 probes after the first),
+// with 4 rows when a group-by sink follows (8 spill registers there); a
+// single remaining probe + a large group-by (TPC-H Q3) runs best one row per
+// lane (profiles/ab_r02_*)
+int auto_drain(const hawk_pipeline& p) {
+  if (p.nprobe < 3) return 1;
+  return p.sink == HAWK_SINK_HASH_AGGREGATE ? 4 : 8;
+}
+
 bool split_rows_for(const hawk_pipeline& pipe, const hawk_variant& v, int role) {
   return v.predication == HAWK_BRANCHED && pipe.nprobe >= 1 &&
          (pipe.nprobe >= 2 || role == hk::K_HAGG_LOCAL || role == hk::K_HAGG_GLOBAL) &&
@@ -339,6 +363,8 @@ int32_t prepare(hawk_ctx* ctx, const hawk_pipeline& pipe, const hawk_variant& v,
   // live-row compaction after the first probe (compiled, branched; the
   // multi-pass roles need CTA-uniform control flow and keep the R-row path)
   kp.split = ctx->jit && ctx->compact && split_rows_for(pipe, v, role);
+  kp.split_drain = !kp.split ? 1 : ctx->drain_rows > 0 ? ctx->drain_rows : auto_drain(pipe);
+  kp.split_bits = kp.split ? ctx->split_bits : 0;
   kp.min_ctas = ctx->min_ctas;
   shape.jit_fn = nullptr;
   if (ctx->jit) {  // compiled program: generate + NVRTC (cached), see jit.cu
@@ -469,7 +495,7 @@ int32_t hawk_b200_ctx_create(int32_t device, hawk_ctx** out) {
   HK_TRY(cudaMalloc(&ctx->d_ctrl, 64));
   HK_TRY(cudaMemset(ctx->d_ctrl, 0, 64));
   HK_TRY(cudaMalloc(&ctx->d_final, HAWK_MAX_AGGS * 8));
-  HK_TRY(cudaMallocHost(&ctx->h_readback, (4 + HAWK_MAX_AGGS) * 8));
+  HK_TRY(cudaMallocHost(&ctx->h_readback, (8 + HAWK_MAX_AGGS) * 8));
   HK_TRY(cudaEventCreate(&ctx->ev0));
   HK_TRY(cudaEventCreate(&ctx->ev1));
   *out = ctx;
@@ -497,6 +523,7 @@ int32_t hawk_b200_ctx_sm_count(hawk_ctx* ctx, int32_t* sms) {
 }
 
 void* hawk_b200_ctx_stream(hawk_ctx* ctx) { return ctx->stream; }
+int32_t hawk_b200_ctx_device(hawk_ctx* ctx) { return ctx ? ctx->device : -1; }
 
 static int main_role(const hawk_pipeline& p, const hawk_variant& v) {
   const bool local = v.strategy == HAWK_LOCAL_HASH, single = v.strategy == HAWK_SINGLE_PASS;
@@ -512,6 +539,8 @@ static void program_params(const hawk_pipeline& p, const hawk_variant& v, hk::KP
   std::memset(&kp, 0, sizeof kp);
   kp.p = p;
   kp.split = split_rows_for(p, v, main_role(p, v));  // the default context options
+  kp.split_drain = kp.split ? auto_drain(p) : 1;
+  kp.split_bits = kp.split ? 1 : 0;
   kp.npre = compile_filters(p.filter, p.nfilter, kp.pre);
   kp.npost = compile_filters(p.post, p.npost, kp.post);
 }
@@ -582,9 +611,37 @@ int32_t hawk_b200_ctx_set_option(hawk_ctx* ctx, const char* name, int64_t value)
     return HAWK_OK;
   }
   if (std::strcmp(name, "priv_groups") == 0) {
-    ctx->priv_groups = (int)std::max<int64_t>(0, std::min<int64_t>(value, 64));
+    ctx->priv_groups = (int)std::max<int64_t>(-1, std::min<int64_t>(value, 64));
     return HAWK_OK;
   }
+  if (std::strcmp(name, "dense_join") == 0) {
+    ctx->dense_join = value != 0;
+    return HAWK_OK;
+  }
+  if (std::strcmp(name, "split_bits") == 0) {
+    ctx->split_bits = (int)std::max<int64_t>(0, std::min<int64_t>(value, 2));
+    return HAWK_OK;
+  }
+  if (std::strcmp(name, "drain_rows") == 0) {
+    ctx->drain_rows = (int)std::max<int64_t>(0, std::min<int64_t>(value, 8));
+    return HAWK_OK;
+  }
+  return HAWK_ERR_ARGUMENT;
+}
+
+int32_t hawk_b200_ctx_get_option(hawk_ctx* ctx, const char* name, int64_t* value) {
+  if (!ctx || !name || !value) return HAWK_ERR_ARGUMENT;
+  const struct { const char* n; int64_t v; } opts[] = {
+      {"prefetch_passes", ctx->prefetch_passes}, {"l2_distance", ctx->l2_distance},
+      {"min_ctas", ctx->min_ctas}, {"compact", ctx->compact}, {"dense_keys", ctx->dense_keys},
+      {"stage_probes", ctx->stage_probes}, {"pass_sync", ctx->pass_sync}, {"jit", ctx->jit},
+      {"stage", ctx->stage}, {"priv_groups", ctx->priv_groups}, {"dense_join", ctx->dense_join},
+      {"drain_rows", ctx->drain_rows}, {"split_bits", ctx->split_bits}};
+  for (const auto& o : opts)
+    if (std::strcmp(name, o.n) == 0) {
+      *value = o.v;
+      return HAWK_OK;
+    }
   return HAWK_ERR_ARGUMENT;
 }
 
@@ -745,7 +802,7 @@ static int32_t insert_launch(hawk_ctx* ctx, const hawk_table* t, const int64_t* 
 }
 
 static int32_t cuckoo_check(hawk_ctx* ctx, const hawk_table* t, int* d_flags) {
-  if (t->impl != HAWK_CUCKOO) return HAWK_OK;
+  if (t->impl != HAWK_CUCKOO || t->d_index != nullptr) return HAWK_OK;
   const int g = grid_for(ctx, t->capacity, 256);
   if (t->function == HAWK_MURMUR)
     hk::cuckoo_duplicate_kernel<HAWK_MURMUR><<<g, 256, 0, ctx->stream>>>(*t, d_flags);
@@ -925,10 +982,47 @@ int32_t hawk_b200_agg_table_merge_rows(hawk_ctx* ctx, const hawk_pipeline* p, ha
   return (h & HAWK_FLAG_TABLE_FULL) ? HAWK_ERR_CAPACITY : HAWK_OK;
 }
 
+int32_t hawk_b200_agg_rows_combine(hawk_ctx* ctx, const hawk_pipeline* p, const int64_t* d_rows,
+                                   int64_t n, int64_t* d_out) {
+  if (!ctx || !p || (!d_rows && n) || !d_out || p->naggs < 0 || p->naggs > HAWK_MAX_AGGS)
+    return HAWK_ERR_ARGUMENT;
+  hk::KParams kp;
+  std::memset(&kp, 0, sizeof kp);
+  kp.p = *p;
+  cudaSetDevice(ctx->device);
+  hk::agg_rows_combine_kernel<<<1, 32, 0, ctx->stream>>>(kp, reinterpret_cast<const u64*>(d_rows), n,
+                                                         reinterpret_cast<u64*>(d_out));
+  HK_TRY(cudaGetLastError());
+  return HAWK_OK;
+}
+
+int32_t hawk_b200_memcpy_d2d(hawk_ctx* ctx, void* d_dst, const void* d_src, size_t bytes) {
+  if (!bytes) return HAWK_OK;
+  HK_TRY(cudaMemcpyAsync(d_dst, d_src, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  return HAWK_OK;
+}
+
 // ---- pipeline execution ----------------------------------------------------------------
+
+static int32_t run_pipeline_impl(hawk_ctx* ctx, const hawk_pipeline* pipe, const hawk_variant* v,
+                                 hawk_output* out, hawk_metrics* metrics, int64_t* h_rows,
+                                 int64_t h_cap_rows);
 
 int32_t hawk_b200_run_pipeline(hawk_ctx* ctx, const hawk_pipeline* pipe, const hawk_variant* v,
                                hawk_output* out, hawk_metrics* metrics) {
+  return run_pipeline_impl(ctx, pipe, v, out, metrics, nullptr, 0);
+}
+
+int32_t hawk_b200_run_pipeline_extract(hawk_ctx* ctx, const hawk_pipeline* pipe, const hawk_variant* v,
+                                       int64_t* h_rows, int64_t h_cap_rows, hawk_output* out,
+                                       hawk_metrics* metrics) {
+  if (!h_rows || h_cap_rows < 0) return HAWK_ERR_ARGUMENT;
+  return run_pipeline_impl(ctx, pipe, v, out, metrics, h_rows, h_cap_rows);
+}
+
+static int32_t run_pipeline_impl(hawk_ctx* ctx, const hawk_pipeline* pipe, const hawk_variant* v,
+                                 hawk_output* out, hawk_metrics* metrics, int64_t* h_rows,
+                                 int64_t h_cap_rows) {
   if (!ctx || !pipe || !v || !out) return HAWK_ERR_ARGUMENT;
   const hawk_pipeline& p = *pipe;
   if (p.nrows < 0 || p.ncolumns > HAWK_MAX_COLUMNS || p.nfilter > HAWK_MAX_FILTERS ||
@@ -1085,15 +1179,43 @@ int32_t hawk_b200_run_pipeline(hawk_ctx* ctx, const hawk_pipeline* pipe, const h
   if (p.sink == HAWK_SINK_HASH_PUT) {
     st = cuckoo_check(ctx, &p.sink_table, d_flags);
     if (st != HAWK_OK) return st;
+    if (p.sink_table.d_index != nullptr) {  // filled entries of the dense index (ctrl word 7)
+      HK_TRY(cudaMemsetAsync(ctx->d_ctrl + 7, 0, 8, ctx->stream));
+      hk::index_fill_count_kernel<<<grid_for(ctx, std::max<int64_t>(p.sink_table.index_span / 4, 1), 256), 256, 0,
+                                    ctx->stream>>>(p.sink_table.d_index, p.sink_table.index_span, ctx->d_ctrl + 7);
+      HK_TRY(cudaGetLastError());
+    }
   }
   HK_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
+  // HASH_AGGREGATE with a host buffer: compact the groups right behind the
+  // pipeline and read up to h_cap_rows of them back with the control words,
+  // so small group-bys (TPC-H Q1: 4 groups) finish with one synchronisation
+  const bool extract = h_rows != nullptr && p.sink == HAWK_SINK_HASH_AGGREGATE;
+  int64_t ex_width = 0, ex_copied = 0;
+  if (extract) {
+    const hawk_table& t = p.sink_table;
+    const int K = p.nkeys, A = p.naggs;
+    ex_width = K + A;
+    const int64_t nslots = t.capacity * (t.impl == HAWK_CUCKOO ? 2 : 1);
+    st = ensure(ctx->d_groups, ctx->groups_cap, (size_t)nslots * ex_width * 8);
+    if (st != HAWK_OK) return st;
+    HK_TRY(cudaMemsetAsync(ctx->d_ctrl + 7, 0, 8, ctx->stream));
+    hk::agg_extract_kernel<<<grid_for(ctx, nslots, 256), 256, 0, ctx->stream>>>(
+        reinterpret_cast<const u64*>(t.d_slots), nslots, K, A, ctx->d_groups, ctx->d_ctrl + 7);
+    HK_TRY(cudaGetLastError());
+    ++nlaunch;
+    ex_copied = std::min(h_cap_rows, nslots);
+    if (ex_copied > 0)
+      HK_TRY(cudaMemcpyAsync(h_rows, ctx->d_groups, (size_t)ex_copied * ex_width * 8, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  }
   const double t_launch = trace ? us_since(t_start) : 0.0;
   // one synchronising read-back: the control words and, for AGGREGATE, the
   // accumulators themselves (pinned)
   u64* ctrl = ctx->h_readback;
-  HK_TRY(cudaMemcpyAsync(ctrl, ctx->d_ctrl, 4 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  HK_TRY(cudaMemcpyAsync(ctrl, ctx->d_ctrl, 8 * 8, cudaMemcpyDeviceToHost, ctx->stream));
   if (p.sink == HAWK_SINK_AGGREGATE && p.naggs > 0)
-    HK_TRY(cudaMemcpyAsync(ctrl + 4, ctx->d_final, (size_t)p.naggs * 8, cudaMemcpyDeviceToHost,
+    HK_TRY(cudaMemcpyAsync(ctrl + 8, ctx->d_final, (size_t)p.naggs * 8, cudaMemcpyDeviceToHost,
                            ctx->stream));
   HK_TRY(cudaStreamSynchronize(ctx->stream));
   float ms = 0.f;
@@ -1107,7 +1229,7 @@ int32_t hawk_b200_run_pipeline(hawk_ctx* ctx, const hawk_pipeline* pipe, const h
   switch (p.sink) {
     case HAWK_SINK_AGGREGATE:
       out->d_values = reinterpret_cast<int64_t*>(ctx->d_final);
-      out->h_values = reinterpret_cast<const int64_t*>(ctrl + 4);
+      out->h_values = reinterpret_cast<const int64_t*>(ctrl + 8);
       out->rows = 1;
       out->width = p.naggs;
       out->stride = p.naggs;
@@ -1115,6 +1237,13 @@ int32_t hawk_b200_run_pipeline(hawk_ctx* ctx, const hawk_pipeline* pipe, const h
     case HAWK_SINK_HASH_AGGREGATE:
       out->rows = (int64_t)ctrl[2];  // groups inserted into the global table
       if ((int64_t)ctrl[2] > kp.group_limit) out->flags |= HAWK_FLAG_TABLE_FULL;
+      if (extract) {  // compacted groups: d_values (all), h_values (when they fit)
+        out->rows = (int64_t)ctrl[7];
+        out->d_values = ctx->d_groups;
+        out->width = (int32_t)ex_width;
+        out->stride = ex_width;
+        out->h_values = out->rows <= ex_copied ? h_rows : nullptr;
+      }
       break;
     case HAWK_SINK_PROJECT:
       out->d_values = ctx->d_out;
@@ -1124,6 +1253,9 @@ int32_t hawk_b200_run_pipeline(hawk_ctx* ctx, const hawk_pipeline* pipe, const h
       break;
     case HAWK_SINK_HASH_PUT:  // rows inserted into the join table
       out->rows = s == HAWK_MULTI_PASS ? rows_written : (int64_t)ctrl[2];
+      // a dense index holds one entry per distinct key: fewer filled entries
+      // than inserted rows means a duplicate build key
+      if (p.sink_table.d_index != nullptr && (int64_t)ctrl[7] != out->rows) out->flags |= HAWK_FLAG_DUPLICATE;
       break;
   }
   if (metrics) {

@@ -72,6 +72,9 @@ __device__ __forceinline__ u64 ldg64_stream(const void* p) {
   asm volatile("ld.global.nc.L1::no_allocate.b64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
 }
+__device__ __forceinline__ void ldg128_stream(const void* p, u64& a, u64& b) {
+  asm volatile("ld.global.nc.L1::no_allocate.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+}
 // probe-side reads of small, hot structures: keep in L1
 __device__ __forceinline__ u64 ldg64_keep(const void* p) {
   u64 v;
@@ -100,6 +103,15 @@ __device__ __forceinline__ u64 ld_acquire_gpu(const u64* p) {
   u64 v;
   asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
+}
+
+__device__ __forceinline__ int ld_acquire_cta_i32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta_i32(int* p, int v) {
+  asm volatile("st.release.cta.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // ---- atomics on generic addresses (smem or HBM) -------------------------------

@@ -13,10 +13,9 @@
 // independent of the program shape.
 //
 // The variant modes are template parameters (one instantiation per point):
-//   ACCESS  COALESCED  — a warp reads 512 contiguous bytes per column load
-//                        (thread t owns rows 2t, 2t+1 of each 2B-row group,
-//                        paper Listing 3 coalesced loop); the CTA's upcoming
-//                        rows are prefetched into L2 with TMA bulk prefetches
+//   ACCESS  COALESCED  — a warp reads 512 contiguous bytes per column load as
+//                        128-bit vectors (thread t owns rows 2t, 2t+1 of each
+//                        2B-row group, paper Listing 3 coalesced loop)
 //           SEQUENTIAL — each thread scans its own contiguous sub-chunk
 //                        (paper "sequential" partitioning)
 //           both read 128-bit vectors (two int64 rows per load)
@@ -90,14 +89,17 @@ struct KParams {
   int32_t split;                      // compiled, branched: compact live rows after the first probe
   int32_t min_ctas;                   // compiled: __launch_bounds__ min CTAs per SM (0 = by unroll)
   int32_t smem_queue_off;             //   ... per-warp queues of (row, probe-0 row id)
+  int32_t split_drain;                //   ... queued rows per lane per drain
+  int32_t split_bits;                 //   ... key bitmaps for semi-join probes: 1 first, 2 all
   int32_t smem_state_off;
   int32_t state_words;                // state words per thread
   int32_t rid_base, key_base, acc_base;
 };
 
 // R rows of one op pass.
-// COALESCED: the pass tile [base, base + B*R) is staged in shared memory by
-//   TMA bulk copies; thread t owns tile rows t + jB (conflict-free LDS).
+// COALESCED: the pass tile [base, base + B*R): thread t owns tile rows
+//   2t + 2pB and 2t + 2pB + 1 for p < R/2, read with 128-bit loads from HBM
+//   (or from the tile staged in shared memory by TMA bulk copies).
 // SEQUENTIAL: thread t owns rows base + j of its own sub-chunk, read from
 //   HBM with 128-bit loads (rows come in aligned pairs).
 // kGather: R explicit rows (the compacted rows of a warp after the first
@@ -111,7 +113,11 @@ struct Batch {
   uint32_t valid;          // rows inside the CTA chunk
   const int64_t* stage;    // COALESCED: this pass's staged tile
   int64_t rows_[ACCESS == kGather ? R : 1];
-  __device__ __forceinline__ int sidx(int j) const { return threadIdx.x + j * B; }
+  // COALESCED: row pair p = j/2 of thread t is tile rows 2t + 2pB, +1, so
+  // every column load of a warp reads 512 contiguous bytes as 128-bit vectors
+  __device__ __forceinline__ int sidx(int j) const {
+    return 2 * (int)threadIdx.x + (j >> 1) * 2 * B + (j & 1);
+  }
   __device__ __forceinline__ int64_t row(int j) const {
     if constexpr (ACCESS == kGather) return rows_[j];
     if (ACCESS == HAWK_COALESCED) return base + sidx(j);
@@ -144,11 +150,18 @@ __device__ __forceinline__ void load_column(const KParams& kp, int slot, const B
 #pragma unroll
     for (int j = 0; j < R; ++j) v[j] = ((b.valid >> j) & 1u) ? ldg64_stream(c + b.row(j)) : 0ull;
   } else if constexpr (ACCESS == HAWK_COALESCED) {
-    if (b.stage) {  // staged tile in shared memory
+    if (b.stage) {  // staged tile in shared memory (128-bit LDS per row pair)
       const int64_t* t = b.stage + (size_t)kp.stage_of[slot] * b.B * R;
 #pragma unroll
-      for (int j = 0; j < R; ++j) v[j] = (u64)t[b.sidx(j)];
-    } else {        // unstaged: warp-coalesced 8-byte loads
+      for (int j = 0; j < R; j += 2) {
+        const longlong2 w = *reinterpret_cast<const longlong2*>(t + b.sidx(j));
+        v[j] = (u64)w.x;
+        v[j + 1] = (u64)w.y;
+      }
+    } else if (b.valid == (1u << R) - 1u) {  // full tile: warp-coalesced 128-bit loads
+#pragma unroll
+      for (int j = 0; j < R; j += 2) ldg128_stream(c + b.row(j), v[j], v[j + 1]);
+    } else {
 #pragma unroll
       for (int j = 0; j < R; ++j) v[j] = ((b.valid >> j) & 1u) ? ldg64_stream(c + b.row(j)) : 0ull;
     }

@@ -139,6 +139,21 @@ __global__ void cuckoo_duplicate_kernel(hawk_table t, int* flags) {
   }
 }
 
+// Filled entries (!= -1) of a dense join index; fewer than the rows the
+// build inserted means a duplicate build key.
+__global__ void index_fill_count_kernel(const int32_t* __restrict__ idx, int64_t span, u64* out) {
+  u64 n = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t quads = span / 4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < quads; i += stride) {
+    const int4 v = __ldg(reinterpret_cast<const int4*>(idx) + i);
+    n += (v.x != -1) + (v.y != -1) + (v.z != -1) + (v.w != -1);
+  }
+  if (blockIdx.x == 0 && threadIdx.x < span - quads * 4) n += idx[quads * 4 + threadIdx.x] != -1;
+  n = __reduce_add_sync(0xffffffffu, (unsigned)n);
+  if ((threadIdx.x & 31) == 0 && n) atomicAdd(out, n);
+}
+
 // ---- aggregation tables -------------------------------------------------------------
 
 // Compacts occupied slots into rows of (keys..., accs...).
@@ -171,6 +186,19 @@ __global__ void agg_merge_rows_kernel(const __grid_constant__ KParams kp, const 
       continue;
     }
     for (int a = 0; a < A; ++a) agg_merge(g + 1 + K + a, p.aggs[a].fn, p.aggs[a].type, r[K + a]);
+  }
+}
+
+// Combines n partial AGGREGATE rows (naggs accumulators each) into one row:
+// the multi-GPU merge of non-grouped aggregates (COUNT partials add).
+__global__ void agg_rows_combine_kernel(const __grid_constant__ KParams kp, const u64* rows,
+                                        int64_t n, u64* out) {
+  const hawk_pipeline& p = kp.p;
+  for (int a = threadIdx.x; a < p.naggs; a += blockDim.x) {
+    const int fn = p.aggs[a].fn == HAWK_COUNT ? HAWK_SUM : p.aggs[a].fn;
+    u64 v = agg_identity(fn, p.aggs[a].type);
+    for (int64_t i = 0; i < n; ++i) v = agg_combine(fn, p.aggs[a].type, v, rows[i * p.naggs + a]);
+    out[a] = v;
   }
 }
 

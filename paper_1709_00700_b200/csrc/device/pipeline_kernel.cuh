@@ -68,6 +68,7 @@ __device__ __forceinline__ void evaluate(const KParams& kp, const Batch<R, ACCES
 struct InterpProg {
   static constexpr bool kStatic = false;  // program shape known only at run time
   static constexpr bool kSplit = false;   // no live-row compaction after the first probe
+  static constexpr int kDrain = 1;        // (queued rows per lane per drain)
   static constexpr int kBlock = 0;        // block size known only at run time
   template <int R>
   struct Vals {};
@@ -228,8 +229,12 @@ __device__ __forceinline__ void hagg_static(const KParams& kp, const Batch<R, AC
             }
             if (in) {
               d = (int)idx;
-              const int o = dense_ord[d];
-              if (o >= 0) target = ((((u64)o * A * B) + threadIdx.x) << 1) | 1ull;
+              const int o = ld_acquire_cta_i32(dense_ord + d);
+              // GP > 0: o is the group's ordinal (thread-private accumulators);
+              // GP == 0: o is its slot in the CTA table (shared-memory atomics)
+              if (o >= 0)
+                target = GP > 0 ? ((((u64)o * A * B) + threadIdx.x) << 1) | 1ull
+                                : ((u64)o << 2) | 2ull;
             }
           }
         }
@@ -243,9 +248,12 @@ __device__ __forceinline__ void hagg_static(const KParams& kp, const Batch<R, AC
               const int o = claim_ordinal(ordinal, si, ord_slot, nord, GP);
               if (o < GP) {
                 target = ((((u64)o * A * B) + threadIdx.x) << 1) | 1ull;
-                if (d >= 0) dense_ord[d] = o;  // every writer stores the same ordinal
+                if (d >= 0) st_release_cta_i32(dense_ord + d, o);  // every writer stores the same ordinal
               }
+            } else if (slot != nullptr && d >= 0) {
+              st_release_cta_i32(dense_ord + d, si);  // every writer stores the same slot
             }
+            if (slot != nullptr && target == 0) target = ((u64)si << 2) | 2ull;  // CTA-table slot
           }
         }
         if (target == 0) {
@@ -263,16 +271,20 @@ __device__ __forceinline__ void hagg_static(const KParams& kp, const Batch<R, AC
     }
     tw[j] = target;
   }
-  // rows with private accumulators (plain shared-memory read-modify-write,
-  // predicated, no branches) and rows updating a table slot with atomics
-  uint32_t pmask = 0, gmask = 0;
+  // target encoding: (offset << 1) | 1 = private accumulators (plain
+  // shared-memory read-modify-write, predicated, no branches); (slot << 2) |
+  // 2 = a CTA-table slot (shared-memory atomics); else a global-table slot
+  // pointer (HBM atomics); 0 = no row
+  uint32_t pmask = 0, smask = 0, gmask = 0;
   u64 off[R];
 #pragma unroll
   for (int j = 0; j < R; ++j) {
     pmask |= (uint32_t)(tw[j] & 1ull) << j;
-    gmask |= (uint32_t)(tw[j] != 0ull && !(tw[j] & 1ull)) << j;
-    off[j] = tw[j] >> 1;
+    smask |= (uint32_t)((tw[j] & 3ull) == 2ull) << j;
+    gmask |= (uint32_t)(tw[j] != 0ull && (tw[j] & 3ull) == 0ull) << j;
+    off[j] = (tw[j] & 1ull) ? tw[j] >> 1 : tw[j] >> 2;
   }
+  const uint32_t local_base = smem_addr(local_table);
   StaticFor<0, A>::run([&](auto ac) {
     constexpr int a = decltype(ac)::value;
     constexpr int fn = P::kAggFn[a], ty = P::kAggType[a];
@@ -291,6 +303,12 @@ __device__ __forceinline__ void hagg_static(const KParams& kp, const Batch<R, AC
         if constexpr (fn == HAWK_COUNT || (fn == HAWK_SUM && ty == HAWK_I64)) acc += v[j];
         else acc = agg_combine(fn, ty, acc, v[j]);
       }
+    }
+    if (smask) {
+#pragma unroll
+      for (int j = 0; j < R; ++j)
+        if ((smask >> j) & 1u)
+          agg_update_smem<fn, ty>(local_base + (uint32_t)((off[j] * (1 + K + A) + 1 + K + a) * 8), v[j]);
     }
     if (gmask) {
 #pragma unroll
@@ -402,16 +420,49 @@ __device__ __forceinline__ void project_static(const KParams& kp, const Batch<R,
 
 // Live-row compaction (compiled, branched): the filters and the first (most
 // selective) probe run on the pass's R rows per thread; the surviving rows of
-// the warp are packed into a per-warp queue (row, probe-0 row id) and the rest
-// of the chain + the sink run on them one row per lane, so the later probes
-// issue instructions for live rows only (SSB Q4.1: 20% of the rows survive the
-// first probe). The compiled eval2 loads every driver column it and the sink
-// need at its start, so the gathers overlap instead of forming a chain of HBM
-// round trips between the probes.
+// the warp are appended to a per-warp queue (row, probe-0 row id) in shared
+// memory. Once the queue holds D rows per lane it is drained: the rest of the
+// chain + the sink run on D queued rows per lane (P::kDrain), so every
+// dependent step of the remaining probe chain (gather the key, look it up,
+// gather the payload) has D independent loads in flight per lane instead of
+// one, and later probes issue instructions for live rows only (SSB Q4.1: 20%
+// of the rows survive the first probe). The tail drains after the LOOP.
+template <class P, int ROLE, int PRED, int IMPL, int HFN, int D, class Sink, class St>
+__device__ __forceinline__ void drain_rows(const KParams& kp, const St& s, uint2* q, uint32_t first,
+                                           uint32_t n, int64_t cb, int B, Sink& sink) {
+  Batch<D, kGather> g;
+  g.base = cb;
+  g.B = B;
+  g.stage = nullptr;
+  g.valid = 0;
+  typename P::template Vals<D> v;
+  const uint32_t lanes = (uint32_t)warp_size_here();
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const uint32_t idx = first + (uint32_t)j * lanes + (uint32_t)lane_id();
+    const bool ok = idx < first + n;
+    const uint2 e = ok ? q[idx] : make_uint2(0u, 0u);
+    g.valid |= (uint32_t)ok << j;
+    g.rows_[j] = cb + (int64_t)e.x;
+    v.p0[j] = (int32_t)e.y;
+  }
+  State<D> s1;
+  s1.ts = s.ts;
+  s1.B = s.B;
+  s1.tid = s.tid;
+  s1.rid_base = s.rid_base;
+  s1.key_base = s.key_base;
+  s1.acc_base = s.acc_base;
+  s1.alive = g.valid;  // (lanes without rows still reach the sink's warp collectives)
+  P::template eval2<kGather, PRED, IMPL, HFN, D>(kp, g, s1, v);
+  sink(g, s1, v);
+}
+
 template <class P, int ROLE, int ACCESS, int PRED, int IMPL, int HFN, int R, class Sink>
 __device__ __forceinline__ void split_rows(const KParams& kp, const Batch<R, ACCESS>& b,
                                            State<R>& s, typename P::template Vals<R>& vals,
-                                           int64_t cb, int B, unsigned char* smem, Sink& sink) {
+                                           int64_t cb, int B, uint2* q, uint32_t& qn, Sink& sink) {
+  constexpr int D = P::kDrain;
   P::template eval1<ACCESS, PRED, IMPL, HFN, R>(kp, b, s, vals);
   const uint32_t alive = s.alive;
   const unsigned mask = warp_mask();
@@ -420,35 +471,36 @@ __device__ __forceinline__ void split_rows(const KParams& kp, const Batch<R, ACC
   const uint32_t incl = warp_incl_scan<uint32_t>(c, mask);
   const uint32_t total = __shfl_sync(mask, incl, last);
   if (total == 0u) return;
-  uint2* q = reinterpret_cast<uint2*>(smem + kp.smem_queue_off) + (threadIdx.x >> 5) * (32 * R);
-  uint32_t pos = incl - c;
+  uint32_t pos = qn + incl - c;
 #pragma unroll
   for (int j = 0; j < R; ++j)
     if ((alive >> j) & 1u) q[pos++] = make_uint2((uint32_t)(b.row(j) - cb), (uint32_t)vals.p0[j]);
+  qn += total;
   __syncwarp(mask);
-  for (uint32_t it = 0; it < total; it += 32u) {
-    const uint32_t idx = it + (uint32_t)lane_id();
-    Batch<1, kGather> g;
-    g.base = cb;
-    g.B = B;
-    g.stage = nullptr;
-    g.valid = idx < total ? 1u : 0u;
-    const uint2 e = g.valid ? q[idx] : make_uint2(0u, 0u);
-    g.rows_[0] = cb + (int64_t)e.x;
-    typename P::template Vals<1> v1;
-    v1.p0[0] = (int32_t)e.y;
-    State<1> s1;
-    s1.ts = s.ts;
-    s1.B = s.B;
-    s1.tid = s.tid;
-    s1.rid_base = s.rid_base;
-    s1.key_base = s.key_base;
-    s1.acc_base = s.acc_base;
-    s1.alive = g.valid;
-    P::template eval2<kGather, PRED, IMPL, HFN, 1>(kp, g, s1, v1);
-    sink(g, s1, v1);
+  const uint32_t batch = (uint32_t)D * (uint32_t)(last + 1);
+  if (qn < batch) return;
+  uint32_t first = 0;
+  while (qn - first >= batch) {
+    drain_rows<P, ROLE, PRED, IMPL, HFN, D>(kp, s, q, first, batch, cb, B, sink);
+    first += batch;
+  }
+  // move the remainder (< one batch) to the front of the queue
+  const uint32_t rest = qn - first;
+  __syncwarp(mask);
+  uint2 tmp[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const uint32_t idx = (uint32_t)j * (uint32_t)(last + 1) + (uint32_t)lane_id();
+    if (idx < rest) tmp[j] = q[first + idx];
   }
   __syncwarp(mask);
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    const uint32_t idx = (uint32_t)j * (uint32_t)(last + 1) + (uint32_t)lane_id();
+    if (idx < rest) q[idx] = tmp[j];
+  }
+  __syncwarp(mask);
+  qn = rest;
 }
 
 template <class P, int ROLE, int ACCESS, int PRED, int IMPL, int HFN, int U>
@@ -526,10 +578,16 @@ __device__ __forceinline__ void pipeline_body(const KParams& kp) {
       project_static<P, AA, PRED, RR>(kp, bb, ss, vv);
     }
   };
+  // live-row compaction queue of this warp (compiled, branched programs)
+  constexpr bool kSplitRows = P::kSplit && PRED == HAWK_BRANCHED &&
+                              (ROLE <= K_HAGG_GLOBAL || ROLE == K_PROJECT_SINGLE);
+  uint2* split_q = reinterpret_cast<uint2*>(smem + kp.smem_queue_off) +
+                   (threadIdx.x >> 5) * (32 * (R + P::kDrain));
+  uint32_t split_n = 0;
   auto process = [&](const Batch<R, ACCESS>& b) {
-    if constexpr (P::kSplit && PRED == HAWK_BRANCHED &&
-                  (ROLE <= K_HAGG_GLOBAL || ROLE == K_PROJECT_SINGLE)) {
-      split_rows<P, ROLE, ACCESS, PRED, IMPL, HFN, R>(kp, b, s, vals, cb, B, smem, sink_static);
+    if constexpr (kSplitRows) {
+      split_rows<P, ROLE, ACCESS, PRED, IMPL, HFN, R>(kp, b, s, vals, cb, B, split_q, split_n,
+                                                      sink_static);
       return;
     }
     P::template eval<ACCESS, PRED, IMPL, HFN, R>(kp, b, s, vals);
@@ -836,6 +894,12 @@ __device__ __forceinline__ void pipeline_body(const KParams& kp) {
       }
       process(b);
     }
+  }
+
+  if constexpr (kSplitRows) {  // rows still queued at the end of the chunk
+    if (split_n > 0u)
+      drain_rows<P, ROLE, PRED, IMPL, HFN, P::kDrain>(kp, s, split_q, 0u, split_n, cb, B, sink_static);
+    __syncwarp(warp_mask());
   }
 
   // ---- sink epilogues ----

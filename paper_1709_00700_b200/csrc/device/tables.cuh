@@ -9,8 +9,15 @@ namespace hk {
 
 // ---- join tables: HASH_PROBE --------------------------
 
+// dense key index (hawk_table.d_index): one 4-byte entry per key of the range
+__device__ __forceinline__ int32_t index_find(const hawk_table& t, u64 key) {
+  const u64 r = key - (u64)t.index_lo;
+  return r < (u64)t.index_span ? __ldg(t.d_index + r) : -1;
+}
+
 template <int IMPL, int HFN>
 __device__ __forceinline__ int32_t table_find(const hawk_table& t, u64 key) {
+  if (t.d_index != nullptr) return index_find(t, key);
   if (key == kEmpty) return -1;
   const u64* s = reinterpret_cast<const u64*>(t.d_slots);
   if (IMPL == HAWK_LINEAR_PROBING) {
@@ -42,6 +49,14 @@ __device__ __forceinline__ int32_t table_find(const hawk_table& t, u64 key) {
 template <int IMPL, int HFN, int R>
 __device__ __forceinline__ void table_find_rows(const hawk_table& t, const u64 (&key)[R],
                                                 uint32_t act, int32_t (&out)[R]) {
+  if (t.d_index != nullptr) {  // dense key range: direct-addressed, R loads in flight
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const u64 r = key[j] - (u64)t.index_lo;
+      out[j] = (((act >> j) & 1u) && r < (u64)t.index_span) ? __ldg(t.d_index + r) : -1;
+    }
+    return;
+  }
   const u64* s = reinterpret_cast<const u64*>(t.d_slots);
   u64 k0[R], v0[R], pos[R];
 #pragma unroll
@@ -81,11 +96,28 @@ __device__ __forceinline__ void table_find_rows(const hawk_table& t, const u64 (
   }
 }
 
+// dense key index insert: a plain store of the build row id into the key's
+// entry. A duplicate build key (planner_reference.cpp:171-174) leaves fewer
+// filled entries than inserted rows, which the build's count pass detects
+// (abi.cu: index_fill_count_kernel), so no atomic is needed per row.
+__device__ __forceinline__ void index_insert(const hawk_table& t, u64 key, u64 payload, int* flags) {
+  const u64 r = key - (u64)t.index_lo;
+  if (r >= (u64)t.index_span) {  // outside the range the index was sized for
+    atomicOr(flags, HAWK_FLAG_TABLE_FULL);
+    return;
+  }
+  t.d_index[r] = (int32_t)payload;
+}
+
 // HASH_PUT: LP = CAS-claim the key slot then store the
 // payload; cuckoo = 128-bit exchange with an eviction chain of <= 32.
 template <int IMPL, int HFN>
 __device__ __forceinline__ void table_insert(const hawk_table& t, u64 key, u64 payload,
                                              int* flags) {
+  if (t.d_index != nullptr) {
+    index_insert(t, key, payload, flags);
+    return;
+  }
   u64* s = reinterpret_cast<u64*>(t.d_slots);
   if (key == kEmpty) {  // the EMPTY sentinel cannot be stored
     atomicOr(flags, HAWK_FLAG_TABLE_FULL);
@@ -127,6 +159,12 @@ template <int IMPL, int HFN, int R>
 __device__ __forceinline__ void table_insert_rows(const hawk_table& t, const u64 (&key)[R],
                                                   const u64 (&payload)[R], uint32_t act,
                                                   int* flags) {
+  if (t.d_index != nullptr) {
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+      if ((act >> j) & 1u) index_insert(t, key[j], payload[j], flags);
+    return;
+  }
   if (IMPL != HAWK_LINEAR_PROBING) {
 #pragma unroll
     for (int j = 0; j < R; ++j)
@@ -246,6 +284,25 @@ __device__ __forceinline__ void agg_update(u64* acc, int fn, int type, u64 v) {
     if (type == HAWK_I64) atomic_min_i(acc, v); else atomic_min_f(acc, as_f64(v));
   } else {
     if (type == HAWK_I64) atomic_max_i(acc, v); else atomic_max_f(acc, as_f64(v));
+  }
+}
+
+// agg_update on a shared-memory accumulator given by its 32-bit shared
+// address: native shared atomics (ATOMS) instead of generic ones
+template <int FN, int TY>
+__device__ __forceinline__ void agg_update_smem(uint32_t a, u64 v) {
+  if constexpr (FN == HAWK_COUNT) {
+    asm volatile("atom.shared.add.u64 %0, [%1], 1;" : "=l"(v) : "r"(a) : "memory");
+  } else if constexpr (FN == HAWK_SUM && TY == HAWK_I64) {
+    asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+  } else if constexpr (FN == HAWK_SUM) {
+    asm volatile("red.shared.add.f64 [%0], %1;" ::"r"(a), "d"(as_f64(v)) : "memory");
+  } else if constexpr (FN == HAWK_MIN && TY == HAWK_I64) {
+    asm volatile("red.shared.min.s64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+  } else if constexpr (FN == HAWK_MAX && TY == HAWK_I64) {
+    asm volatile("red.shared.max.s64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+  } else {  // f64 MIN / MAX: CAS loop on the generic address
+    agg_update(reinterpret_cast<u64*>(__cvta_shared_to_generic(a)), FN, TY, v);
   }
 }
 

@@ -221,6 +221,24 @@ int32_t hawk_engine_run_partial(hawk_engine* e, const char* sql, const char* con
   });
 }
 
+int32_t hawk_engine_run_sharded(hawk_engine* e, const char* sql, const char* config, hawk_comm* comm,
+                                int32_t root, hawk_result** out) {
+  *out = nullptr;
+  return guard([&] {
+    const PipelineSet& set = cached_plan(e, sql);
+    WorkloadConfig w = config && *config ? parse_workload_config(config) : WorkloadConfig();
+    auto* r = new hawk_result;
+    try {
+      r->table = e->engine.execute_sharded(set, w, comm, root, &r->metrics);
+    } catch (...) {
+      delete r;
+      throw;
+    }
+    fill_metrics_text(r);
+    *out = r;
+  });
+}
+
 int64_t hawk_partial_rows(const hawk_partial* p) { return p->part.rows; }
 int32_t hawk_partial_width(const hawk_partial* p) { return p->part.width; }
 int32_t hawk_partial_sink(const hawk_partial* p) { return p->part.sink; }

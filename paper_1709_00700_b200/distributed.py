@@ -20,6 +20,18 @@ def shard_range(n: int, rank: int, world: int, align: int = 64) -> tuple[int, in
     return b, min(n, b + per)
 
 
+def copartition_range(lineitem_begin: int, lineitem_end: int) -> tuple[int, int]:
+    """The orders rows holding exactly the orderkeys of lineitem rows
+    [begin, end): l_orderkey = i / 4 + 1 and o_orderkey = j + 1
+    (include/hawk_gen.h), so lineitem shard boundaries that are multiples of
+    4 cut orders at [begin / 4, end / 4). Each rank then builds the orders
+    join table of its own shard only, and every lineitem row finds its order
+    on its own GPU (TPC-H Q3)."""
+    if lineitem_begin % 4 or (lineitem_end % 4 and lineitem_end != lineitem_begin):
+        raise ValueError("lineitem shard boundaries must be multiples of 4")
+    return lineitem_begin // 4, lineitem_end // 4
+
+
 def all_gather_rows(parts: np.ndarray, device=None) -> list[np.ndarray]:
     """All-gathers a (rows x width) int64 block from every rank (variable rows)."""
     import torch

@@ -272,6 +272,15 @@ class Engine:
         _check(self._lib.hawk_engine_run(self._h, sql.encode(), config.encode(), C.byref(r)))
         return _result_from(self._lib, r)  # frees r when the columns are gone
 
+    def run_sharded(self, sql: str, config: str, comm: "Communicator", root: int = 0) -> Result:
+        """Multi-GPU: this rank's shard, NCCL gather of the partials to `root`
+        over device buffers, device merge (Engine::execute_sharded). Non-root
+        ranks get the query's columns with no rows."""
+        r = C.c_void_p()
+        _check(self._lib.hawk_engine_run_sharded(self._h, sql.encode(), config.encode(), comm.handle,
+                                                 root, C.byref(r)))
+        return _result_from(self._lib, r)
+
     def run_partial(self, sql: str, config: str = "") -> "Partial":
         """Shard execution: the (rows x width) int64 partials before the cross-GPU merge."""
         p = C.c_void_p()
@@ -352,3 +361,41 @@ class Engine:
         _check(self._lib.hawk_engine_learn(self._h, arr, len(sqls), q, prune_ms, reps, buf, 512,
                                            C.byref(ms), C.byref(ev), C.byref(sw)))
         return dict(config=buf.value.decode(), ms=ms.value, evaluations=ev.value, sweeps=sw.value)
+
+
+class Communicator:
+    """An NCCL communicator on an engine's device (include/hawk_b200_comm.h).
+    `unique_id` (128 bytes) comes from Communicator.unique_id() on one rank and
+    is shipped to the others by the launcher (torch.distributed in bench.py)."""
+
+    def __init__(self, engine: Engine, world: int, rank: int, unique_id: bytes):
+        lib = _native.b200()
+        if not lib.hawk_nccl_available():
+            raise Unsupported("libnccl.so.2 is not available")
+        self._lib = lib
+        h = C.c_void_p()
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        st = lib.hawk_nccl_comm_create(engine.ctx, world, rank, buf, C.byref(h))
+        if st != 0:
+            raise HawkError(f"ncclCommInitRank failed: status {st}")
+        self.handle = h
+        self.world, self.rank = world, rank
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        st = _native.b200().hawk_nccl_unique_id(buf)
+        if st != 0:
+            raise HawkError(f"ncclGetUniqueId failed: status {st}")
+        return bytes(buf)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.hawk_nccl_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -27,6 +27,9 @@ MINMAX = ("select l_returnflag, l_linestatus, sum(l_quantity) as q, min(l_extend
 def _case(name):
     from paper_1709_00700_b200 import datagen as dg
     from paper_1709_00700_b200 import queries as Q
+    if name == "tpch_q3_copartitioned":
+        sql, tables, fact = Q.BENCH["tpch_q3"]
+        return sql, tables, fact, [0, 2, 3], [(1, 0, 0)]
     # (key positions, [(agg position, fn, type)]) with SUM=0 COUNT=1 MIN=2 MAX=3, I64=0
     if name == "minmax":
         return MINMAX, [dg.LINEITEM], dg.LINEITEM, [0, 1], [(2, 0, 0), (3, 2, 0), (4, 3, 0), (5, 1, 0)]
@@ -49,7 +52,8 @@ def _worker(rank, world, port, name, sf, seed, failures):
     sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
     from oracle_bridge import OraDb, OraTable
     from paper_1709_00700_b200 import datagen as dg
-    from paper_1709_00700_b200.distributed import all_gather_rows, merge_partials_host, shard_range
+    from paper_1709_00700_b200.distributed import (all_gather_rows, copartition_range,
+                                                   merge_partials_host, shard_range)
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
         sql, tables, fact, keys, aggs = _case(name)
@@ -59,6 +63,10 @@ def _worker(rank, world, port, name, sf, seed, failures):
         for t in tables:
             if t == fact:
                 tname, cols = dg.host_table(t, sf, seed, b, e - b)
+            elif name == "tpch_q3_copartitioned" and t == dg.ORDERS:
+                # orders co-partitioned with the lineitem shard (bench.py load_tables)
+                ob, oe = copartition_range(b, e)
+                tname, cols = dg.host_table(t, sf, seed, ob, oe - ob)
             else:
                 tname, cols = dg.host_table(t, sf, seed)
             db.add(OraTable.from_columns(tname, cols))
@@ -87,7 +95,8 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("name", ["tpch_q6", "ssb_q11", "ssb_q41", "tpch_q3", "minmax"])
+@pytest.mark.parametrize("name", ["tpch_q6", "ssb_q11", "ssb_q41", "tpch_q3", "tpch_q3_copartitioned",
+                                  "minmax"])
 def test_sharded_partials_merge_to_oracle(name):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
@@ -128,3 +137,16 @@ def test_merge_partials_host_semantics():
     empty = np.zeros((0, 2), np.int64)
     m = merge_partials_host(1, [(0, 0)], 1, [g1, empty, g2])
     assert m.tolist() == [[1, 11], [2, 5], [3, 0]]
+
+
+def test_copartition_range():
+    from paper_1709_00700_b200 import datagen as dg
+    from paper_1709_00700_b200.distributed import copartition_range, shard_range
+    n = dg.table_rows(dg.LINEITEM, 0.01)
+    for world in (2, 3, 8):
+        spans = [copartition_range(*shard_range(n, r, world)) for r in range(world)]
+        assert spans[0][0] == 0 and spans[-1][1] == dg.table_rows(dg.ORDERS, 0.01)
+        for (b0, e0), (b1, _) in zip(spans, spans[1:]):
+            assert e0 == b1
+    with pytest.raises(ValueError):
+        copartition_range(2, 8)

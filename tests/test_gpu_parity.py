@@ -161,6 +161,41 @@ def test_sharded_partials_finalize_to_oracle(key, world):
         e.close()
 
 
+@pytest.mark.parametrize("key", sorted(Q.BENCH))
+def test_nccl_sharded_execution_one_rank(key):
+    # the multi-GPU data path end to end on one GPU: Engine.run_sharded keeps
+    # the partials in HBM, gathers them to the root with NCCL over device
+    # buffers (a one-rank communicator here) and merges them on the device
+    from paper_1709_00700_b200 import Communicator
+    sql, tables, fact = Q.BENCH[key]
+    e = Engine(0)
+    try:
+        for t in tables:
+            e.generate(t, 0.01, 42)
+        comm = Communicator(e, 1, 0, Communicator.unique_id())
+        db = harness.oracle_db(harness.bench_tables("ssb" if key.startswith("ssb") else "tpch", 0.01, 42))
+        for cfg in (CONFIGS[0], CONFIGS[1]):
+            diff = harness.compare(db.execute(sql), e.run_sharded(sql, cfg, comm))
+            assert diff is None, f"{key} [{cfg}]: {diff}"
+        comm.close()
+    finally:
+        e.close()
+
+
+def test_nccl_sharded_projection_and_empty(micro):
+    from paper_1709_00700_b200 import Communicator
+    engine, db = micro
+    comm = Communicator(engine, 1, 0, Communicator.unique_id())
+    try:
+        for sql in (Q.LISTING1, Q.LISTING2, "select sum(lo_quantity), count(*) from lineorder where lo_quantity > 100"):
+            diff = harness.compare(db.execute(sql), engine.run_sharded(sql, CONFIGS[0], comm))
+            assert diff is None, f"{sql}: {diff}"
+        with pytest.raises(EmptyAggregate):
+            engine.run_sharded("select min(lo_quantity) from lineorder where lo_quantity > 100", CONFIGS[0], comm)
+    finally:
+        comm.close()
+
+
 def test_column_range(engine):
     lib = _native.b200()
     rng = np.random.default_rng(5)
