@@ -116,6 +116,38 @@ int32_t hawk_engine_learn(hawk_engine* e, const char* const* sqls, int32_t n, in
                           double prune_ms, int32_t reps, char* best, int32_t len, double* best_ms,
                           int32_t* evaluations, int32_t* sweeps);
 
+/* Learned-configuration files: key=value, one dimension per
+ * line ("projection.strategy=single_pass", ...). load writes the
+ * configuration in to_string() form ("<proj>;<agg>") into buf. */
+int32_t hawk_config_save(const char* config, const char* path);
+int32_t hawk_config_load(const char* path, char* buf, int32_t len);
+
+/* full_exploration of one pipeline kind's variant space
+ * (kind 0: the 32 projection variants, 1: the 896 aggregation variants), the
+ * other kind fixed by `fixed` ("<proj>;<agg>", "" = default). Writes the
+ * ranking-order trace as CSV to csv_path (NULL = none): index, projection,
+ * aggregation, ms, status (ok / pruned / error), detail. */
+int32_t hawk_engine_explore(hawk_engine* e, const char* const* sqls, int32_t n, int32_t kind,
+                            const char* fixed, double prune_ms, int32_t reps, const char* csv_path,
+                            char* best, int32_t len, double* best_ms, int32_t* evaluations);
+/* learn_variant_configuration with every option: early termination, an
+ * unroll pass after the descent, '|'-separated start configurations (NULL =
+ * the reference default), the measurement trace as CSV and the learned
+ * configuration as a key-value file (NULL paths = not written). */
+int32_t hawk_engine_learn_ex(hawk_engine* e, const char* const* sqls, int32_t n, int32_t q,
+                             int32_t early_termination, double prune_ms, int32_t reps,
+                             int32_t unroll_pass, const char* starts, const char* trace_csv_path,
+                             const char* config_path, char* best, int32_t len, double* best_ms,
+                             int32_t* evaluations, int32_t* sweeps);
+
+/* Algorithm 1 over an abstract space: dimension d has sizes[d] values;
+ * cost(index vector) may return INFINITY. Measurements are cached by index
+ * vector; best receives ndims indices. */
+typedef double (*hawk_index_cost_fn)(const int32_t* index, int32_t ndims, void* user);
+int32_t hawk_coordinate_descent(int32_t ndims, const int32_t* sizes, hawk_index_cost_fn cost, void* user,
+                                int32_t q, int32_t early_termination, int32_t* best, double* best_ms,
+                                int32_t* evaluations, int32_t* sweeps, int32_t* sweep1_evaluations);
+
 /* Algorithm 1 over a caller-supplied cost: cost(config)
  * returns the time of a workload configuration in to_string() format
  * (INFINITY = failed/pruned). No engine or GPU involved. */

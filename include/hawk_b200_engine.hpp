@@ -259,6 +259,9 @@ struct LearnOptions {
   bool early_termination = true;     // stop at the first unchanged sweep
   double prune_threshold_ms = 1000;  // slow-variant pruning
   int repetitions = 3;               // timed runs per query (median)
+  /// After the descent, one coordinate pass over the projection and
+  /// aggregation unroll factors {1, 2, 4} (outside the 32 / 896 space).
+  bool unroll_pass = false;
   /// Starting configurations of the descent (Algorithm 1 line 1). Empty =
   /// the reference's default VariantConfiguration (every dimension's first
   /// value); more than one = restarts sharing one measurement cache, best
@@ -299,6 +302,18 @@ struct LearnResult {
 /// by configuration key, strict-< keeps the earlier value.
 LearnResult learn_variant_configuration(Engine& engine, const std::vector<WorkloadQuery>& workload,
                                         const LearnOptions& opt);
+/// Algorithm 1 over an abstract index space: dimension d takes values
+/// 0..sizes[d]-1 in feature order; measurements cached by index vector.
+struct IndexDescent {
+  std::vector<int> best;
+  double best_ms = std::numeric_limits<double>::infinity();
+  int evaluations = 0;
+  int sweeps = 0;
+  std::vector<int> evaluations_per_sweep;
+};
+IndexDescent descend(const std::vector<int>& sizes, const LearnOptions& opt,
+                     const std::vector<std::vector<int>>& starts,
+                     const std::function<double(const std::vector<int>&)>& cost);
 /// Algorithm 1 over any cost function (the learner above with `cost` =
 /// measure_variant); used directly by the CPU tests with synthetic costs.
 LearnResult coordinate_descent(const std::vector<Dimension>& dims, const LearnOptions& opt,
@@ -310,6 +325,9 @@ WorkloadConfig b200_start_config();
 LearnResult full_exploration(Engine& engine, const std::vector<WorkloadQuery>& workload,
                              const std::vector<WorkloadConfig>& space, const LearnOptions& opt);
 
+/// The exploration / learning trace as CSV: index, projection, aggregation,
+/// ms (inf = failed or pruned), status (ok / pruned / error), detail.
+std::string trace_csv(const std::vector<Measurement>& trace);
 /// Offline heuristic file: one `key=value` per line.
 std::string save_config_text(const WorkloadConfig& c);
 WorkloadConfig load_config_text(const std::string& text);

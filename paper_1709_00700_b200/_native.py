@@ -160,12 +160,22 @@ def engine() -> C.CDLL:
              C.POINTER(f64), C.POINTER(i32), C.POINTER(i32))
         _sig(lib, "hawk_learn_with_cost", i32, COST_FN, vp, i32, i32, cp, cp, i32, C.POINTER(f64),
              C.POINTER(i32), C.POINTER(i32))
+        _sig(lib, "hawk_config_save", i32, cp, cp)
+        _sig(lib, "hawk_config_load", i32, cp, cp, i32)
+        _sig(lib, "hawk_engine_explore", i32, vp, C.POINTER(cp), i32, i32, cp, f64, i32, cp, cp, i32,
+             C.POINTER(f64), C.POINTER(i32))
+        _sig(lib, "hawk_engine_learn_ex", i32, vp, C.POINTER(cp), i32, i32, i32, f64, i32, i32, cp, cp,
+             cp, cp, i32, C.POINTER(f64), C.POINTER(i32), C.POINTER(i32))
+        _sig(lib, "hawk_coordinate_descent", i32, i32, C.POINTER(i32), INDEX_COST_FN, vp, i32, i32,
+             C.POINTER(i32), C.POINTER(f64), C.POINTER(i32), C.POINTER(i32), C.POINTER(i32))
         _engine = lib
     return _engine
 
 
 # double (*hawk_cost_fn)(const char* config, void* user)
 COST_FN = C.CFUNCTYPE(C.c_double, C.c_char_p, C.c_void_p)
+# double (*hawk_index_cost_fn)(const int32_t* index, int32_t ndims, void* user)
+INDEX_COST_FN = C.CFUNCTYPE(C.c_double, C.POINTER(C.c_int32), C.c_int32, C.c_void_p)
 
 
 def declared_symbols(header: str) -> list[str]:

@@ -128,10 +128,16 @@ __device__ __forceinline__ u64* agg_find_static(const KParams& kp, u64* slots, i
   const u64 h = HFN == HAWK_MURMUR ? fmix64(x ^ seeds[0]) : ms_multiplier(seeds[0]) * x;
   const u64 tag = h | 1ull;
   const u64 cap = 1ull << log2cap;
-  const int max_tries = IMPL == HAWK_LINEAR_PROBING ? (int)(cap < 4096 ? cap : 4096) : 2;
-  u64 pos = HFN == HAWK_MURMUR ? (h & (cap - 1ull)) : (h >> (64 - log2cap));
+  // cuckoo aggregation tables are bucketised: each of the two candidate
+  // positions opens a run of kAggBucket slots (groups are never moved, since
+  // other threads update their accumulators in place)
+  const int max_tries = IMPL == HAWK_LINEAR_PROBING ? (int)(cap < 4096 ? cap : 4096) : 2 * kAggBucket;
+  const u64 home = HFN == HAWK_MURMUR ? (h & (cap - 1ull)) : (h >> (64 - log2cap));
+  u64 pos = home;
   for (int t = 0; t < max_tries; ++t) {
-    if (IMPL == HAWK_CUCKOO && t == 1) pos = cap + hash_slot<HFN>(x, seeds[1], log2cap);
+    if (IMPL == HAWK_CUCKOO)
+      pos = t < kAggBucket ? ((home + (u64)t) & (cap - 1ull))
+                           : cap + ((hash_slot<HFN>(x, seeds[1], log2cap) + (u64)(t - kAggBucket)) & (cap - 1ull));
     u64* sl = slots + pos * (u64)words;
     u64 st = SHARED ? ld_acquire_cta(sl) : ld_acquire_gpu(sl);
     if (st == 0ull) {
@@ -229,7 +235,10 @@ __device__ __forceinline__ void hagg_static(const KParams& kp, const Batch<R, AC
             }
             if (in) {
               d = (int)idx;
-              const int o = ld_acquire_cta_i32(dense_ord + d);
+              // GP > 0: private accumulators are thread-owned and need no
+              // ordering; GP == 0: the CTA slot's contents must be visible
+              const int o = GP > 0 ? *reinterpret_cast<volatile int*>(dense_ord + d)
+                                   : ld_acquire_cta_i32(dense_ord + d);
               // GP > 0: o is the group's ordinal (thread-private accumulators);
               // GP == 0: o is its slot in the CTA table (shared-memory atomics)
               if (o >= 0)
@@ -253,7 +262,9 @@ __device__ __forceinline__ void hagg_static(const KParams& kp, const Batch<R, AC
             } else if (slot != nullptr && d >= 0) {
               st_release_cta_i32(dense_ord + d, si);  // every writer stores the same slot
             }
-            if (slot != nullptr && target == 0) target = ((u64)si << 2) | 2ull;  // CTA-table slot
+            // GP == 0: a CTA-table slot (shared-memory atomics); GP > 0 keeps
+            // its rare ordinal-overflow rows on the generic path below
+            if (slot != nullptr && target == 0 && GP == 0) target = ((u64)si << 2) | 2ull;
           }
         }
         if (target == 0) {
@@ -280,9 +291,9 @@ __device__ __forceinline__ void hagg_static(const KParams& kp, const Batch<R, AC
 #pragma unroll
   for (int j = 0; j < R; ++j) {
     pmask |= (uint32_t)(tw[j] & 1ull) << j;
-    smask |= (uint32_t)((tw[j] & 3ull) == 2ull) << j;
+    if (GP == 0) smask |= (uint32_t)((tw[j] & 3ull) == 2ull) << j;
     gmask |= (uint32_t)(tw[j] != 0ull && (tw[j] & 3ull) == 0ull) << j;
-    off[j] = (tw[j] & 1ull) ? tw[j] >> 1 : tw[j] >> 2;
+    off[j] = tw[j] >> 1;
   }
   const uint32_t local_base = smem_addr(local_table);
   StaticFor<0, A>::run([&](auto ac) {
@@ -308,7 +319,7 @@ __device__ __forceinline__ void hagg_static(const KParams& kp, const Batch<R, AC
 #pragma unroll
       for (int j = 0; j < R; ++j)
         if ((smask >> j) & 1u)
-          agg_update_smem<fn, ty>(local_base + (uint32_t)((off[j] * (1 + K + A) + 1 + K + a) * 8), v[j]);
+          agg_update_smem<fn, ty>(local_base + (uint32_t)(((tw[j] >> 2) * (1 + K + A) + 1 + K + a) * 8), v[j]);
     }
     if (gmask) {
 #pragma unroll

@@ -217,6 +217,8 @@ __device__ __forceinline__ void table_insert_rows(const hawk_table& t, const u64
 
 // ---- aggregation tables: {state, keys..., accs...} slots --------
 
+constexpr int kAggBucket = 8;  // slots per cuckoo candidate position
+
 __host__ __device__ __forceinline__ u64 agg_identity(int fn, int type) {
   if (fn == HAWK_MIN) return type == HAWK_I64 ? 0x7fffffffffffffffull : 0x7ff0000000000000ull;
   if (fn == HAWK_MAX) return type == HAWK_I64 ? 0x8000000000000000ull : 0xfff0000000000000ull;
@@ -242,10 +244,16 @@ __device__ __forceinline__ u64* agg_find_or_insert(const KParams& kp, u64* slots
   const u64 h = HFN == HAWK_MURMUR ? fmix64(x ^ seeds[0]) : ms_multiplier(seeds[0]) * x;
   const u64 tag = h | 1ull;
   const u64 cap = 1ull << log2cap;
-  const int max_tries = IMPL == HAWK_LINEAR_PROBING ? (int)(cap < 4096 ? cap : 4096) : 2;
-  u64 pos = HFN == HAWK_MURMUR ? (h & (cap - 1ull)) : (h >> (64 - log2cap));
+  // cuckoo aggregation tables are bucketised: each of the two candidate
+  // positions opens a run of kAggBucket slots (groups are never moved, since
+  // other threads update their accumulators in place)
+  const int max_tries = IMPL == HAWK_LINEAR_PROBING ? (int)(cap < 4096 ? cap : 4096) : 2 * kAggBucket;
+  const u64 home = HFN == HAWK_MURMUR ? (h & (cap - 1ull)) : (h >> (64 - log2cap));
+  u64 pos = home;
   for (int t = 0; t < max_tries; ++t) {
-    if (IMPL == HAWK_CUCKOO && t == 1) pos = cap + hash_slot<HFN>(x, seeds[1], log2cap);
+    if (IMPL == HAWK_CUCKOO)
+      pos = t < kAggBucket ? ((home + (u64)t) & (cap - 1ull))
+                           : cap + ((hash_slot<HFN>(x, seeds[1], log2cap) + (u64)(t - kAggBucket)) & (cap - 1ull));
     u64* sl = slots + pos * (u64)words;
     u64 st = SHARED ? ld_acquire_cta(sl) : ld_acquire_gpu(sl);
     if (st == 0ull) {

@@ -1,6 +1,7 @@
 // capi.cpp — extern "C" wrapper of the C++ engine (include/hawk_b200_engine.h).
 // No exception crosses this boundary: each is mapped to its hawk_status class.
 #include <cstring>
+#include <fstream>
 #include <sstream>
 #include <unordered_map>
 
@@ -443,6 +444,111 @@ int32_t hawk_engine_learn(hawk_engine* e, const char* const* sqls, int32_t n, in
     *best_ms = r.best_ms;
     *evaluations = r.evaluations;
     *sweeps = r.sweeps;
+  });
+}
+
+static void write_file(const char* path, const std::string& text) {
+  if (!path || !*path) return;
+  std::ofstream f(path, std::ios::binary);
+  if (!f) throw Error(std::string("cannot write ") + path);
+  f << text;
+  if (!f) throw Error(std::string("cannot write ") + path);
+}
+
+int32_t hawk_config_save(const char* config, const char* path) {
+  return guard([&] { write_file(path, save_config_text(parse_workload_config(config ? config : ""))); });
+}
+
+int32_t hawk_config_load(const char* path, char* buf, int32_t len) {
+  return guard([&] {
+    std::ifstream f(path ? path : "");
+    if (!f) throw InvalidParams(std::string("cannot read config file ") + (path ? path : ""));
+    std::stringstream ss;
+    ss << f.rdbuf();
+    put_str(buf, len, load_config_text(ss.str()).to_string());
+  });
+}
+
+static std::vector<WorkloadQuery> workload_of(const char* const* sqls, int32_t n) {
+  if (n < 1) throw InvalidParams("empty workload");
+  std::vector<WorkloadQuery> w;
+  for (int i = 0; i < n; ++i) w.push_back({"q" + std::to_string(i), sqls[i]});
+  return w;
+}
+
+int32_t hawk_engine_explore(hawk_engine* e, const char* const* sqls, int32_t n, int32_t kind,
+                            const char* fixed, double prune_ms, int32_t reps, const char* csv_path,
+                            char* best, int32_t len, double* best_ms, int32_t* evaluations) {
+  return guard([&] {
+    const auto w = workload_of(sqls, n);
+    const WorkloadConfig base = fixed && *fixed ? parse_workload_config(fixed) : WorkloadConfig();
+    PipelineProgram shape;
+    shape.kind = kind == 0 ? PipelineKind::Projection : PipelineKind::Aggregation;
+    std::vector<WorkloadConfig> space;
+    for (const VariantConfiguration& v : enumerate_variant_space(shape)) {
+      WorkloadConfig c = base;
+      (kind == 0 ? c.projection : c.aggregation) = v;
+      space.push_back(c);
+    }
+    LearnOptions opt;
+    opt.prune_threshold_ms = prune_ms;
+    opt.repetitions = reps;
+    LearnResult r = full_exploration(e->engine, w, space, opt);
+    write_file(csv_path, trace_csv(r.trace));
+    put_str(best, len, r.best.to_string());
+    *best_ms = r.best_ms;
+    *evaluations = r.evaluations;
+  });
+}
+
+int32_t hawk_engine_learn_ex(hawk_engine* e, const char* const* sqls, int32_t n, int32_t q,
+                             int32_t early_termination, double prune_ms, int32_t reps,
+                             int32_t unroll_pass, const char* starts, const char* trace_csv_path,
+                             const char* config_path, char* best, int32_t len, double* best_ms,
+                             int32_t* evaluations, int32_t* sweeps) {
+  return guard([&] {
+    const auto w = workload_of(sqls, n);
+    LearnOptions opt;
+    opt.max_iterations = q;
+    opt.early_termination = early_termination != 0;
+    opt.prune_threshold_ms = prune_ms;
+    opt.repetitions = reps;
+    opt.unroll_pass = unroll_pass != 0;
+    if (starts && *starts) {
+      std::stringstream ss(starts);
+      std::string part;
+      while (std::getline(ss, part, '|')) opt.starts.push_back(parse_workload_config(part));
+    }
+    LearnResult r = learn_variant_configuration(e->engine, w, opt);
+    write_file(trace_csv_path, trace_csv(r.trace));
+    write_file(config_path, save_config_text(r.best));
+    put_str(best, len, r.best.to_string());
+    *best_ms = r.best_ms;
+    *evaluations = r.evaluations;
+    *sweeps = r.sweeps;
+  });
+}
+
+int32_t hawk_coordinate_descent(int32_t ndims, const int32_t* sizes, hawk_index_cost_fn cost, void* user,
+                                int32_t q, int32_t early_termination, int32_t* best, double* best_ms,
+                                int32_t* evaluations, int32_t* sweeps, int32_t* sweep1_evaluations) {
+  return guard([&] {
+    if (ndims < 1 || !sizes || !cost || !best) throw InvalidParams("coordinate descent: bad arguments");
+    std::vector<int> sz(sizes, sizes + ndims);
+    for (int v : sz)
+      if (v < 1) throw InvalidParams("coordinate descent: empty dimension");
+    LearnOptions opt;
+    opt.max_iterations = q;
+    opt.early_termination = early_termination != 0;
+    IndexDescent r = descend(sz, opt, {}, [&](const std::vector<int>& idx) {
+      std::vector<int32_t> i32(idx.begin(), idx.end());
+      return cost(i32.data(), ndims, user);
+    });
+    for (int d = 0; d < ndims; ++d) best[d] = r.best.empty() ? 0 : r.best[static_cast<std::size_t>(d)];
+    *best_ms = r.best_ms;
+    *evaluations = r.evaluations;
+    *sweeps = r.sweeps;
+    if (sweep1_evaluations) *sweep1_evaluations = r.evaluations_per_sweep.empty() ? 0 : r.evaluations_per_sweep[0];
   });
 }
 

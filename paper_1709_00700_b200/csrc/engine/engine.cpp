@@ -8,6 +8,8 @@
 #include <malloc.h>
 #include <mutex>
 #include <chrono>
+#include <condition_variable>
+#include <functional>
 #include <limits>
 #include <cstdio>
 #include <cstdlib>
@@ -112,7 +114,7 @@ struct Engine::Impl {
   // groups the last run of a terminal program produced (keyed by the program
   // inside a cached PipelineSet): sizes the aggregation table and the
   // speculative read-back of the next run
-  std::unordered_map<const void*, int64_t> group_hint;
+  std::unordered_map<std::string, int64_t> group_hint;
 
   void* acquire(size_t bytes) {
     auto it = pool.lower_bound(bytes);
@@ -476,23 +478,85 @@ Value decode_value(const PipelineSet& set, const OutputColumn& oc, int64_t raw) 
   return raw;
 }
 
-// Splits [0, n) over host threads for large results (TPC-H Q3 SF100 returns
-// 1.2M groups: a single thread reading the DMA-written rows is memory bound).
+// A persistent pool of host threads for large results (TPC-H Q3 SF100
+// returns 1.2M groups): spawning threads per call cost more than the copy.
+class HostPool {
+ public:
+  HostPool() {
+    const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    const int n = std::min(hw, 16) - 1;
+    for (int i = 0; i < n; ++i) workers_.emplace_back([this, i] { loop(i + 1); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> l(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (std::thread& t : workers_) t.join();
+  }
+  int size() const { return static_cast<int>(workers_.size()) + 1; }
+  // runs f(b, e) on T contiguous chunks of [0, n); the caller takes chunk 0
+  void run(int64_t n, int T, const std::function<void(int64_t, int64_t)>& f) {
+    std::lock_guard<std::mutex> one_task(run_mu_);  // engines on other threads queue up
+    std::unique_lock<std::mutex> l(mu_);
+    task_ = &f;
+    n_ = n;
+    T_ = T;
+    pending_ = T - 1;
+    ++gen_;
+    l.unlock();
+    cv_.notify_all();
+    f(0, std::min(n, chunk()));
+    l.lock();
+    done_.wait(l, [&] { return pending_ == 0; });
+    task_ = nullptr;
+  }
+
+ private:
+  int64_t chunk() const { return (n_ + T_ - 1) / T_; }
+  void loop(int id) {
+    uint64_t seen = 0;
+    for (;;) {
+      std::unique_lock<std::mutex> l(mu_);
+      cv_.wait(l, [&] { return stop_ || gen_ != seen; });
+      if (stop_) return;
+      seen = gen_;
+      if (id >= T_) continue;
+      const std::function<void(int64_t, int64_t)>* f = task_;
+      const int64_t c = chunk(), b = std::min(n_, id * c), e = std::min(n_, b + c);
+      l.unlock();
+      (*f)(b, e);
+      l.lock();
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex run_mu_, mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int64_t, int64_t)>* task_ = nullptr;
+  int64_t n_ = 0;
+  int T_ = 1, pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+HostPool& host_pool() {
+  static HostPool pool;
+  return pool;
+}
+
+// Splits [0, n) over the host pool for large results.
 template <typename F>
 void parallel_rows(int64_t n, F&& f) {
   const int64_t per_thread = 1 << 15;
-  const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
-  const int T = static_cast<int>(std::min<int64_t>(std::min(hw, 16), (n + per_thread - 1) / per_thread));
+  HostPool& pool = host_pool();
+  const int T = static_cast<int>(std::min<int64_t>(pool.size(), (n + per_thread - 1) / per_thread));
   if (T <= 1) {
     f(0, n);
     return;
   }
-  std::vector<std::thread> pool;
-  const int64_t chunk = (n + T - 1) / T;
-  for (int t = 1; t < T; ++t)
-    pool.emplace_back([&, t] { f(std::min(n, t * chunk), std::min(n, (t + 1) * chunk)); });
-  f(0, std::min(n, chunk));
-  for (std::thread& th : pool) th.join();
+  pool.run(n, T, std::function<void(int64_t, int64_t)>(f));
 }
 
 // HostFinalize: AVG division, output schema in SELECT order,
@@ -1052,7 +1116,10 @@ static QueryRun run_query(Engine& e, Engine::Impl& I, const PipelineSet& set,
     pm.rows_in = driver.rows;
     hawk_output out{};
     const bool grouped = lp.pipe.sink == HAWK_SINK_HASH_AGGREGATE;
-    const void* hint_key = &set.pipelines[T];
+    // keyed by the lowered program and its driver table (plan objects are
+    // recycled, their addresses are no key)
+    const std::string hint_key = driver.name + "#" + std::to_string(driver.rows) + "#" +
+                                 std::to_string(driver.row_offset) + "\n" + describe(lp.pipe);
     auto hint_it = I.group_hint.find(hint_key);
     const int64_t hint = hint_it == I.group_hint.end() ? -1 : hint_it->second;
     int64_t bound = grouped ? I.groups_bound(lp, set, driver.rows) : 0;
@@ -1094,7 +1161,11 @@ static QueryRun run_query(Engine& e, Engine::Impl& I, const PipelineSet& set,
         // group count is bounded by the input rows, so this terminates
         const int64_t need = std::max<int64_t>(bound * 4, out.rows * 2);
         if (bound >= std::max<int64_t>(driver.rows, 1) || attempt >= 8)
-          throw CapacityExceeded("aggregation table overflowed at " + std::to_string(bound) + " groups");
+          throw CapacityExceeded("aggregation table overflowed at a bound of " + std::to_string(bound) +
+                                 " groups (" + std::to_string(lp.pipe.sink_table.capacity) + " slots" +
+                                 (v.hash_table_impl == HAWK_CUCKOO ? " per cuckoo sub-table" : "") + ", " +
+                                 std::to_string(out.rows) + " groups extracted, attempt " +
+                                 std::to_string(attempt) + ")");
         bound = std::min<int64_t>(need, std::max<int64_t>(driver.rows, 1));
         ++pm.retries;
         continue;

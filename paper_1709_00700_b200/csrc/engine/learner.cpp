@@ -5,6 +5,7 @@
 #include <cmath>
 #include <functional>
 #include <map>
+#include <sstream>
 
 #include "hawk/sql/parser.hpp"
 #include "hawk_b200_engine.hpp"
@@ -26,6 +27,19 @@ std::vector<PreparedQuery> prepare(Engine& engine, const std::vector<WorkloadQue
     out.push_back({q.name, partition_into_pipelines(plan, tables)});
   }
   return out;
+}
+
+// the reference exception class of a failed measurement (hawk/error.hpp:9-54)
+std::string error_class(const std::exception& e) {
+  if (dynamic_cast<const CapacityExceeded*>(&e)) return "CapacityExceeded";
+  if (dynamic_cast<const DuplicateKey*>(&e)) return "DuplicateKey";
+  if (dynamic_cast<const PlanTooLarge*>(&e)) return "PlanTooLarge";
+  if (dynamic_cast<const InvalidConfig*>(&e)) return "InvalidConfig";
+  if (dynamic_cast<const Unsupported*>(&e)) return "Unsupported";
+  if (dynamic_cast<const UnsupportedPlan*>(&e)) return "UnsupportedPlan";
+  if (dynamic_cast<const EmptyAggregate*>(&e)) return "EmptyAggregate";
+  if (dynamic_cast<const DivergentPlan*>(&e)) return "DivergentPlan";
+  return "Error";
 }
 
 std::vector<VariantConfiguration> per_kind(const PipelineSet& set, const WorkloadConfig& c) {
@@ -52,8 +66,8 @@ Measurement measure(Engine& engine, const WorkloadConfig& config,
         if (em.kernel_ms > opt.prune_threshold_ms) break;
       }
     } catch (const std::exception& e) {
-      // variant errors count as +inf
-      m.error = q.name + ": " + e.what();
+      // variant errors count as +inf with a diagnostic
+      m.error = q.name + ": " + error_class(e) + ": " + e.what();
       m.ms = std::numeric_limits<double>::infinity();
       return m;
     }
@@ -82,54 +96,32 @@ WorkloadConfig b200_start_config() {
       "single_pass/coalesced/branched;local_hash/coalesced/branched/linear_probing/murmur/wg=256/ht=8");
 }
 
-LearnResult coordinate_descent(const std::vector<Dimension>& dims, const LearnOptions& opt,
-                               const std::function<Measurement(const WorkloadConfig&)>& cost) {
-  LearnResult res;
-  auto config_of = [&](const std::vector<int>& idx) {
-    WorkloadConfig c;
-    for (std::size_t d = 0; d < dims.size(); ++d) dims[d].set(c, idx[d]);
-    return c;
-  };
-  // dimension value indices of a configuration (values not on a dimension's
-  // list fall back to its first value)
-  auto index_of = [&](const WorkloadConfig& c) {
-    std::vector<int> idx(dims.size(), 0);
-    for (std::size_t d = 0; d < dims.size(); ++d)
-      for (int v = 0; v < static_cast<int>(dims[d].values.size()); ++v) {
-        WorkloadConfig t = c;
-        dims[d].set(t, v);
-        if (t.to_string() == c.to_string()) {
-          idx[d] = v;
-          break;
-        }
-      }
-    return idx;
-  };
-  std::map<std::string, Measurement> cache;  // measurements by configuration key
+IndexDescent descend(const std::vector<int>& sizes, const LearnOptions& opt,
+                     const std::vector<std::vector<int>>& starts_in,
+                     const std::function<double(const std::vector<int>&)>& cost) {
+  IndexDescent res;
+  std::map<std::vector<int>, double> cache;  // measurements by configuration
   auto eval = [&](const std::vector<int>& idx) -> double {
-    WorkloadConfig c = config_of(idx);
-    const std::string key = c.to_string();
-    auto it = cache.find(key);
-    if (it != cache.end()) return it->second.ms;
-    Measurement m = cost(c);
-    m.config = c;
+    auto it = cache.find(idx);
+    if (it != cache.end()) return it->second;
+    const double ms = cost(idx);
     ++res.evaluations;
-    res.trace.push_back(m);
-    cache[key] = m;
-    return m.ms;
+    if (!res.evaluations_per_sweep.empty()) ++res.evaluations_per_sweep.back();
+    cache[idx] = ms;
+    return ms;
   };
-  std::vector<std::vector<int>> starts;
-  if (opt.starts.empty()) starts.emplace_back(dims.size(), 0);  // Algorithm 1 line 1
-  for (const WorkloadConfig& c : opt.starts) starts.push_back(index_of(c));
+  std::vector<std::vector<int>> starts = starts_in;
+  if (starts.empty()) starts.emplace_back(sizes.size(), 0);  // Algorithm 1 line 1
   bool first = true;
   for (std::vector<int> cur : starts) {
     int sweeps = 0;
     for (int sweep = 0; sweep < opt.max_iterations; ++sweep) {
+      res.evaluations_per_sweep.push_back(0);
       bool changed = false;
-      for (std::size_t d = 0; d < dims.size(); ++d) {   // feature order
+      for (std::size_t d = 0; d < sizes.size(); ++d) {  // feature order
         int best_v = cur[d];
         double best = eval(cur);
-        for (int v = 0; v < static_cast<int>(dims[d].values.size()); ++v) {
+        for (int v = 0; v < sizes[d]; ++v) {
           std::vector<int> cand = cur;
           cand[d] = v;
           const double ms = eval(cand);
@@ -148,7 +140,7 @@ LearnResult coordinate_descent(const std::vector<Dimension>& dims, const LearnOp
     }
     const double ms = eval(cur);
     if (first || ms < res.best_ms) {
-      res.best = config_of(cur);
+      res.best = cur;
       res.best_ms = ms;
       res.sweeps = sweeps;
     }
@@ -157,12 +149,119 @@ LearnResult coordinate_descent(const std::vector<Dimension>& dims, const LearnOp
   return res;
 }
 
+LearnResult coordinate_descent(const std::vector<Dimension>& dims, const LearnOptions& opt,
+                               const std::function<Measurement(const WorkloadConfig&)>& cost) {
+  LearnResult res;
+  auto config_of = [&](const std::vector<int>& idx) {
+    WorkloadConfig c;
+    if (!opt.starts.empty()) c = opt.starts.front();  // fields outside the dimensions
+    for (std::size_t d = 0; d < dims.size(); ++d) dims[d].set(c, idx[d]);
+    return c;
+  };
+  // dimension value indices of a configuration (values not on a dimension's
+  // list fall back to its first value)
+  auto index_of = [&](const WorkloadConfig& c) {
+    std::vector<int> idx(dims.size(), 0);
+    for (std::size_t d = 0; d < dims.size(); ++d)
+      for (int v = 0; v < static_cast<int>(dims[d].values.size()); ++v) {
+        WorkloadConfig t = c;
+        dims[d].set(t, v);
+        if (t.to_string() == c.to_string()) {
+          idx[d] = v;
+          break;
+        }
+      }
+    return idx;
+  };
+  // distinct index vectors can name one configuration (e.g. thread
+  // multipliers of a single-pass projection): measure each configuration once
+  std::map<std::string, double> by_config;
+  std::vector<int> sizes;
+  for (const Dimension& d : dims) sizes.push_back(static_cast<int>(d.values.size()));
+  std::vector<std::vector<int>> starts;
+  for (const WorkloadConfig& c : opt.starts) starts.push_back(index_of(c));
+  IndexDescent r = descend(sizes, opt, starts, [&](const std::vector<int>& idx) {
+    const WorkloadConfig c = config_of(idx);
+    const std::string key = c.to_string();
+    auto it = by_config.find(key);
+    if (it != by_config.end()) return it->second;
+    Measurement m = cost(c);
+    m.config = c;
+    ++res.evaluations;
+    res.trace.push_back(m);
+    by_config[key] = m.ms;
+    return m.ms;
+  });
+  res.best = config_of(r.best);
+  res.best_ms = r.best_ms;
+  res.sweeps = r.sweeps;
+  return res;
+}
+
+std::vector<Dimension> unroll_dimensions() {
+  std::vector<Dimension> dims;
+  for (int kind = 0; kind < 2; ++kind) {
+    Dimension d{kind == 0 ? "projection_unroll" : "aggregation_unroll", {}, nullptr};
+    for (int u : kUnrollFactors) d.values.push_back(std::to_string(u));
+    d.set = [kind](WorkloadConfig& c, int v) {
+      (kind == 0 ? c.projection : c.aggregation).unroll_factor = kUnrollFactors[v];
+    };
+    dims.push_back(d);
+  }
+  return dims;
+}
+
 LearnResult learn_variant_configuration(Engine& engine, const std::vector<WorkloadQuery>& workload,
                                         const LearnOptions& opt) {
   const std::vector<PreparedQuery> queries = prepare(engine, workload);
-  return coordinate_descent(workload_dimensions(), opt, [&](const WorkloadConfig& c) {
-    return measure(engine, c, queries, opt);
-  });
+  auto cost = [&](const WorkloadConfig& c) { return measure(engine, c, queries, opt); };
+  LearnResult res = coordinate_descent(workload_dimensions(), opt, cost);
+  if (!opt.unroll_pass || !std::isfinite(res.best_ms)) return res;
+  // unroll is a code transformation outside the 32 / 896 space:
+  // one coordinate pass over the projection and aggregation unroll factors,
+  // starting from the learned configuration
+  std::vector<Dimension> dims = unroll_dimensions();
+  for (Dimension& d : dims) {
+    auto set = d.set;
+    const WorkloadConfig base = res.best;
+    d.set = [set, base](WorkloadConfig& c, int v) {
+      const int pu = c.projection.unroll_factor, au = c.aggregation.unroll_factor;
+      c = base;
+      c.projection.unroll_factor = pu;
+      c.aggregation.unroll_factor = au;
+      set(c, v);
+    };
+  }
+  LearnOptions uo = opt;
+  uo.max_iterations = 1;
+  uo.starts = {res.best};
+  LearnResult u = coordinate_descent(dims, uo, cost);
+  res.evaluations += u.evaluations;
+  for (Measurement& m : u.trace) res.trace.push_back(std::move(m));
+  if (u.best_ms < res.best_ms) {
+    res.best = u.best;
+    res.best_ms = u.best_ms;
+  }
+  return res;
+}
+
+// Exploration / learning trace as CSV (config fields + metric
+// columns): one row per measured configuration, in measurement order.
+std::string trace_csv(const std::vector<Measurement>& trace) {
+  std::ostringstream os;
+  os << "index,projection,aggregation,ms,status,detail\n";
+  int i = 0;
+  for (const Measurement& m : trace) {
+    std::string detail = m.error;
+    for (char& ch : detail)
+      if (ch == '"' || ch == '\n' || ch == '\r') ch = '\'';
+    const char* status = !m.error.empty() ? "error" : m.pruned ? "pruned" : "ok";
+    os << i++ << "," << m.config.projection.to_string() << "," << m.config.aggregation.to_string() << ",";
+    if (std::isfinite(m.ms)) os << m.ms;
+    else os << "inf";
+    os << "," << status << ",\"" << detail << "\"\n";
+  }
+  return os.str();
 }
 
 LearnResult full_exploration(Engine& engine, const std::vector<WorkloadQuery>& workload,

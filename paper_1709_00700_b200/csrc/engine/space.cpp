@@ -203,10 +203,26 @@ std::vector<Dimension> workload_dimensions() {
   return dims;
 }
 
+// The learned-configuration file ("key-value text file, one
+// dimension per line"): every field of both pipeline kinds' variant.
 std::string save_config_text(const WorkloadConfig& c) {
   std::ostringstream os;
-  os << "projection=" << c.projection.to_string() << "\n";
-  os << "aggregation=" << c.aggregation.to_string() << "\n";
+  os << "# hawk-b200 variant configuration: <pipeline kind>.<dimension>=<value>\n";
+  for (const auto& [kind, v] : {std::pair<const char*, const VariantConfiguration*>{"projection", &c.projection},
+                                {"aggregation", &c.aggregation}}) {
+    const auto parts = split(v->to_string(), '/');
+    os << kind << ".strategy=" << parts[0] << "\n";
+    os << kind << ".memory_access=" << parts[1] << "\n";
+    os << kind << ".predication=" << parts[2] << "\n";
+    os << kind << ".hash_table_impl="
+       << (v->hash_table_impl == HashTableImpl::Cuckoo ? "cuckoo" : "linear_probing") << "\n";
+    os << kind << ".hash_function="
+       << (v->hash_function == HashFunctionKind::MultiplyShift ? "multiply_shift" : "murmur") << "\n";
+    os << kind << ".thread_multiplier=" << v->thread_multiplier << "\n";
+    os << kind << ".work_group_size=" << v->work_group_size << "\n";
+    os << kind << ".hash_table_count_multiplier=" << v->hash_table_count_multiplier << "\n";
+    os << kind << ".unroll_factor=" << v->unroll_factor << "\n";
+  }
   return os.str();
 }
 
@@ -214,15 +230,59 @@ WorkloadConfig load_config_text(const std::string& text) {
   WorkloadConfig w;
   std::istringstream is(text);
   std::string line;
+  auto number = [](const std::string& key, const std::string& v) {
+    try {
+      std::size_t used = 0;
+      const int n = std::stoi(v, &used);
+      if (used != v.size()) throw std::invalid_argument(v);
+      return n;
+    } catch (const std::exception&) {
+      throw InvalidConfig("config key '" + key + "': '" + v + "' is not an integer");
+    }
+  };
   while (std::getline(is, line)) {
+    while (!line.empty() && (line.back() == '\r' || line.back() == ' ')) line.pop_back();
+    if (line.empty() || line[0] == '#') continue;
     auto eq = line.find('=');
-    if (eq == std::string::npos) continue;
+    if (eq == std::string::npos) throw InvalidConfig("config line '" + line + "': expected key=value");
     std::string key = line.substr(0, eq), value = line.substr(eq + 1);
-    while (!value.empty() && (value.back() == '\r' || value.back() == ' ')) value.pop_back();
-    if (key == "projection") w.projection = parse_variant(value);
-    else if (key == "aggregation") w.aggregation = parse_variant(value);
-    else throw InvalidConfig("unknown config key '" + key + "'");
+    if (key == "projection") {  // whole-variant form: projection=<to_string()>
+      w.projection = parse_variant(value);
+      continue;
+    }
+    if (key == "aggregation") {
+      w.aggregation = parse_variant(value);
+      continue;
+    }
+    const auto dot = key.find('.');
+    const std::string kind = dot == std::string::npos ? "" : key.substr(0, dot);
+    const std::string dim = dot == std::string::npos ? key : key.substr(dot + 1);
+    VariantConfiguration* v = kind == "projection" ? &w.projection : kind == "aggregation" ? &w.aggregation : nullptr;
+    if (!v) throw InvalidConfig("unknown config key '" + key + "'");
+    if (dim == "strategy") {
+      v->strategy = parse_variant(value + "/sequential/branched").strategy;
+    } else if (dim == "memory_access") {
+      v->memory_access = parse_variant("single_pass/" + value + "/branched").memory_access;
+    } else if (dim == "predication") {
+      v->predication = parse_variant("single_pass/sequential/" + value).predication;
+    } else if (dim == "hash_table_impl") {
+      v->hash_table_impl = parse_variant("single_pass/sequential/branched/" + value).hash_table_impl;
+    } else if (dim == "hash_function") {
+      v->hash_function = parse_variant("single_pass/sequential/branched/" + value).hash_function;
+    } else if (dim == "thread_multiplier") {
+      v->thread_multiplier = number(key, value);
+    } else if (dim == "work_group_size") {
+      v->work_group_size = number(key, value);
+    } else if (dim == "hash_table_count_multiplier") {
+      v->hash_table_count_multiplier = number(key, value);
+    } else if (dim == "unroll_factor") {
+      v->unroll_factor = number(key, value);
+    } else {
+      throw InvalidConfig("unknown config key '" + key + "'");
+    }
   }
+  // the parsed text must name an admissible configuration (value lists)
+  parse_workload_config(w.to_string());
   return w;
 }
 

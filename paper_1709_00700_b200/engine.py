@@ -354,6 +354,34 @@ class Engine:
                                              reps, C.byref(ms)))
         return ms.value
 
+    def explore(self, sqls: list[str], kind: str = "aggregation", fixed: str = "",
+                prune_ms: float = 1000.0, reps: int = 1, csv_path: str | None = None) -> dict:
+        """full_exploration of one pipeline kind's space (32 projection / 896
+        aggregation variants), the other kind fixed; CSV trace to csv_path."""
+        arr = (C.c_char_p * len(sqls))(*[s.encode() for s in sqls])
+        buf = C.create_string_buffer(512)
+        ms, ev = C.c_double(), C.c_int32()
+        _check(self._lib.hawk_engine_explore(self._h, arr, len(sqls), 0 if kind == "projection" else 1,
+                                             fixed.encode(), prune_ms, reps,
+                                             csv_path.encode() if csv_path else None, buf, 512,
+                                             C.byref(ms), C.byref(ev)))
+        return dict(config=buf.value.decode(), ms=ms.value, evaluations=ev.value)
+
+    def learn_ex(self, sqls: list[str], q: int = 3, early: bool = True, prune_ms: float = 1000.0,
+                 reps: int = 3, unroll_pass: bool = True, starts: list[str] | None = None,
+                 trace_csv: str | None = None, config_path: str | None = None) -> dict:
+        """Algorithm 1 with the unroll pass, restarts, and the trace CSV /
+        key-value config file outputs."""
+        arr = (C.c_char_p * len(sqls))(*[s.encode() for s in sqls])
+        buf = C.create_string_buffer(512)
+        ms, ev, sw = C.c_double(), C.c_int32(), C.c_int32()
+        _check(self._lib.hawk_engine_learn_ex(
+            self._h, arr, len(sqls), q, int(early), prune_ms, reps, int(unroll_pass),
+            "|".join(starts).encode() if starts else None, trace_csv.encode() if trace_csv else None,
+            config_path.encode() if config_path else None, buf, 512, C.byref(ms), C.byref(ev),
+            C.byref(sw)))
+        return dict(config=buf.value.decode(), ms=ms.value, evaluations=ev.value, sweeps=sw.value)
+
     def learn(self, sqls: list[str], q: int = 3, prune_ms: float = 1000.0, reps: int = 3) -> dict:
         arr = (C.c_char_p * len(sqls))(*[s.encode() for s in sqls])
         buf = C.create_string_buffer(512)
@@ -399,3 +427,15 @@ class Communicator:
             self.close()
         except Exception:
             pass
+
+
+def save_config(config: str, path: str):
+    """Writes a workload configuration ("<proj>;<agg>") as the key-value
+    learned-configuration file."""
+    _check(_native.engine().hawk_config_save(config.encode(), path.encode()))
+
+
+def load_config(path: str) -> str:
+    buf = C.create_string_buffer(512)
+    _check(_native.engine().hawk_config_load(path.encode(), buf, 512))
+    return buf.value.decode()

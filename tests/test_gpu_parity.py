@@ -6,6 +6,7 @@ within 1e-9 relative, compared with the reference's own compare_result_tables.
 """
 import ctypes as C
 import json
+import math
 import os
 import struct
 
@@ -584,3 +585,32 @@ def test_cross_expand_kernel(engine, n_driver, n_aux):
         lib.hawk_b200_free(ctx, d_out)
     assert lib.hawk_b200_cross_expand(ctx, None, C.c_int64(1), C.c_int64(1), 0, d_out) != 0
     assert lib.hawk_b200_cross_expand(ctx, d_src, C.c_int64(1), C.c_int64(1), 2, d_out) != 0
+
+
+def test_learner_within_125_of_full_exploration(micro, tmp_path):
+    # SPEC.md:545 (acceptance 6): the configuration Algorithm 1 learns on the
+    # B200 costs at most 1.25x the best of the full exploration of the 896
+    # aggregation variants, with far fewer measurements; the learned
+    # configuration returns the oracle's rows
+    engine, db = micro
+    engine.set_option("jit", 1)
+    sqls = [Q.LISTING8, Q.LISTING9]
+    start = "single_pass/coalesced/branched;local_hash/coalesced/branched/linear_probing/murmur/wg=256/ht=8"
+    learned = engine.learn_ex(sqls, q=3, reps=3, unroll_pass=True,
+                              starts=["single_pass/sequential/branched;local_hash/sequential/branched/"
+                                      "linear_probing/murmur/wg=16/ht=1", start],
+                              trace_csv=str(tmp_path / "learn.csv"), config_path=str(tmp_path / "learned.conf"))
+    full = engine.explore(sqls, "aggregation", fixed=learned["config"].split(";")[0] + ";", reps=3,
+                          csv_path=str(tmp_path / "explore.csv"))
+    assert full["evaluations"] == 896
+    assert learned["evaluations"] < 896
+    assert math.isfinite(learned["ms"]) and learned["ms"] <= 1.25 * full["ms"], (learned, full)
+    rows = open(tmp_path / "explore.csv").read().splitlines()
+    assert rows[0].startswith("index,projection,aggregation,ms,status") and len(rows) == 897
+    from paper_1709_00700_b200.engine import load_config
+    cfg = load_config(str(tmp_path / "learned.conf"))
+    assert cfg == learned["config"]
+    for sql in sqls:
+        diff = harness.compare(db.execute(sql), engine.run(sql, cfg))
+        assert diff is None, f"{sql} [{cfg}]: {diff}"
+    engine.set_option("jit", 0)
