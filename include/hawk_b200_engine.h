@@ -46,6 +46,11 @@ int32_t hawk_engine_put_columns(hawk_engine* e, const char* name, int32_t ncols,
 /* synthetic table generated in HBM (include/hawk_gen.h); rows < 0 = all */
 int32_t hawk_engine_generate(hawk_engine* e, int32_t table, double sf, uint64_t seed,
                              int64_t row_begin, int64_t rows);
+/* CSV file -> device columns (include/hawk_b200_csv.h; the reference's
+ * load_csv rules, storage_csv.cpp:111-155); kinds as above */
+int32_t hawk_engine_load_csv(hawk_engine* e, const char* path, const char* name, int32_t ncols,
+                             const char* const* names, const int32_t* kinds, char delimiter,
+                             int32_t header);
 int32_t hawk_engine_drop(hawk_engine* e, const char* name);
 int64_t hawk_engine_table_rows(hawk_engine* e, const char* name);
 /* device pointer of a stored column (for direct kernel tests) */

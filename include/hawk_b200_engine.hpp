@@ -32,6 +32,7 @@
 #include "hawk/ir/passes.hpp"
 #include "hawk/ir/program.hpp"
 #include "hawk/planner/pipelines.hpp"
+#include "hawk/storage/csv.hpp"
 #include "hawk/storage/table.hpp"
 #include "hawk_b200.h"
 #include "hawk_b200_comm.h"
@@ -154,6 +155,10 @@ class Engine {
   /// (include/hawk_gen.h) directly in HBM; `rows` < 0 = the whole table.
   void generate_table(int hg_table, double sf, uint64_t seed, int64_t row_begin = 0,
                       int64_t rows = -1);
+  /// CSV file -> device columns, parsed on the device with the reference's
+  /// load_csv rules (storage_csv.cpp:111-155; include/hawk_b200_csv.h).
+  void load_csv(const std::string& path, const std::string& name, const Schema& schema,
+                const CsvOptions& options = {});
   void drop_table(const std::string& name);
   bool has_table(const std::string& name) const;
   const DeviceTable& table(const std::string& name) const;

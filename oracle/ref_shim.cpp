@@ -14,6 +14,7 @@
 //   result_checksum             /root/reference/proj/src/planner_result.cpp:86-112
 //   gen_lineorder/part/supplier /root/reference/proj/src/storage_generator.cpp:33-103
 //   partition_into_pipelines    /root/reference/proj/src/planner_pipelines.cpp:550-554
+//   load_csv                    /root/reference/proj/src/storage_csv.cpp:111-155
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -25,6 +26,7 @@
 #include "hawk/planner/reference.hpp"
 #include "hawk/planner/result.hpp"
 #include "hawk/sql/parser.hpp"
+#include "hawk/storage/csv.hpp"
 #include "hawk/storage/generator.hpp"
 
 namespace {
@@ -110,6 +112,22 @@ OraTable* ora_table_gen(const char* which, int64_t n, uint64_t seed, char* err, 
                         ? hawk::gen_supplier(static_cast<std::size_t>(n), seed)
                         : throw hawk::Error("unknown generator " + w);
     return new OraTable{std::make_shared<hawk::Table>(std::move(t))};
+  } catch (const std::exception& e) {
+    put_err(err, errlen, e.what());
+    return nullptr;
+  }
+}
+
+// the reference's load_csv (storage_csv.cpp:111-155); kinds as ora_table_new
+OraTable* ora_table_load_csv(const char* path, const char* name, int ncols, const char* const* names,
+                             const int* kinds, char delimiter, int header, char* err, int errlen) {
+  try {
+    hawk::Schema schema;
+    for (int c = 0; c < ncols; ++c) schema.push_back({names[c], static_cast<hawk::ColumnKind>(kinds[c])});
+    hawk::CsvOptions opt;
+    opt.delimiter = delimiter;
+    opt.header = header != 0;
+    return new OraTable{std::make_shared<hawk::Table>(hawk::load_csv(path, name, schema, opt))};
   } catch (const std::exception& e) {
     put_err(err, errlen, e.what());
     return nullptr;

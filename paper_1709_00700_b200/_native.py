@@ -88,6 +88,16 @@ def b200() -> C.CDLL:
         _sig(lib, "hawk_b200_mem_info", i32, vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t))
         _sig(lib, "hawk_b200_ctx_get_option", i32, vp, cp, C.POINTER(i64))
         _sig(lib, "hawk_b200_ctx_device", i32, vp)
+        # include/hawk_b200_csv.h
+        _sig(lib, "hawk_b200_csv_open", i32, vp, vp, i64, C.c_char, i32, C.POINTER(vp))
+        _sig(lib, "hawk_b200_csv_rows", i64, vp)
+        _sig(lib, "hawk_b200_csv_parse", i32, vp, i32, C.POINTER(i32), C.POINTER(vp), C.POINTER(i64),
+             C.POINTER(i32))
+        _sig(lib, "hawk_b200_csv_error", cp, vp)
+        _sig(lib, "hawk_b200_csv_lexicon_size", i64, vp, i32)
+        _sig(lib, "hawk_b200_csv_lexicon", cp, vp, i32, i64)
+        _sig(lib, "hawk_b200_csv_host_parsed", i32, vp)
+        _sig(lib, "hawk_b200_csv_close", i32, vp)
         # include/hawk_b200_comm.h
         _sig(lib, "hawk_nccl_available", i32)
         _sig(lib, "hawk_nccl_unique_id", i32, vp)
@@ -126,6 +136,7 @@ def engine() -> C.CDLL:
         _sig(lib, "hawk_engine_run", i32, vp, cp, cp, C.POINTER(vp))
         _sig(lib, "hawk_engine_run_partial", i32, vp, cp, cp, C.POINTER(vp))
         _sig(lib, "hawk_engine_run_sharded", i32, vp, cp, cp, vp, i32, C.POINTER(vp))
+        _sig(lib, "hawk_engine_load_csv", i32, vp, cp, cp, i32, C.POINTER(cp), C.POINTER(i32), C.c_char, i32)
         _sig(lib, "hawk_partial_rows", i64, vp)
         _sig(lib, "hawk_partial_width", i32, vp)
         _sig(lib, "hawk_partial_sink", i32, vp)

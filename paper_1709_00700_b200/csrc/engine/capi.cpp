@@ -52,6 +52,8 @@ int32_t classify(const std::exception& e) {
   if (dynamic_cast<const UnknownTable*>(&e)) return 11;
   if (dynamic_cast<const UnknownAttribute*>(&e)) return 12;
   if (dynamic_cast<const TypeError*>(&e)) return 13;
+  if (dynamic_cast<const ParseError*>(&e)) return 14;
+  if (dynamic_cast<const IoError*>(&e)) return 15;
   return 99;
 }
 
@@ -163,6 +165,20 @@ int32_t hawk_engine_put_columns(hawk_engine* e, const char* name, int32_t ncols,
 int32_t hawk_engine_generate(hawk_engine* e, int32_t table, double sf, uint64_t seed,
                              int64_t row_begin, int64_t rows) {
   return guard([&] { e->engine.generate_table(table, sf, seed, row_begin, rows); });
+}
+
+int32_t hawk_engine_load_csv(hawk_engine* e, const char* path, const char* name, int32_t ncols,
+                             const char* const* names, const int32_t* kinds, char delimiter,
+                             int32_t header) {
+  return guard([&] {
+    if (ncols < 1 || !names || !kinds) throw InvalidParams("load_csv: no columns");
+    Schema schema;
+    for (int i = 0; i < ncols; ++i) schema.push_back({names[i], static_cast<ColumnKind>(kinds[i])});
+    CsvOptions opt;
+    opt.delimiter = delimiter;
+    opt.header = header != 0;
+    e->engine.load_csv(path, name, schema, opt);
+  });
 }
 
 int32_t hawk_engine_drop(hawk_engine* e, const char* name) {

@@ -9,7 +9,9 @@
 #include <mutex>
 #include <chrono>
 #include <condition_variable>
+#include <fstream>
 #include <functional>
+#include <iterator>
 #include <limits>
 #include <cstdio>
 #include <cstdlib>
@@ -24,6 +26,8 @@
 #include "hawk_gen.h"
 #include "hawk_b200_cross.h"
 #include "hawk_b200_comm.h"
+#include "hawk_b200_csv.h"
+#include "hawk/storage/csv.hpp"
 
 namespace hawk::b200 {
 
@@ -429,6 +433,82 @@ void Engine::generate_table(int hg_table, double sf, uint64_t seed, int64_t row_
   impl_->tables[name] = std::move(dt);
 }
 
+// CSV ingest: the file's bytes go to HBM once and are
+// parsed there (include/hawk_b200_csv.h) with the reference's load_csv rules
+// (storage_csv.cpp:111-155). Inputs the device parser hands back — a quote
+// inside an unquoted field, which the parallel record scan cannot follow, or
+// a malformed field whose ParseError must carry the reference's line and
+// column — go through the reference's own load_csv, then H2D.
+void Engine::load_csv(const std::string& path, const std::string& name, const Schema& schema,
+                      const CsvOptions& options) {
+  require_device(ctx_);
+  if (schema.empty() || schema.size() > 64) throw SchemaMismatch("load_csv: 1..64 columns");
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw IoError("cannot open '" + path + "'");
+  std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  hawk_csv* csv = nullptr;
+  check(hawk_b200_csv_open(ctx_, text.data(), static_cast<int64_t>(text.size()), options.delimiter,
+                           options.header ? 1 : 0, &csv),
+        "CSV scan");
+  struct Closer {
+    hawk_csv* c;
+    ~Closer() { hawk_b200_csv_close(c); }
+  } closer{csv};
+  const int64_t rows = hawk_b200_csv_rows(csv);
+  ++generation_;
+  drop_table(name);
+  DeviceTable dt;
+  dt.name = name;
+  dt.rows = rows;
+  std::vector<int32_t> kinds;
+  std::vector<int64_t*> cols;
+  const size_t bytes = static_cast<size_t>(padded_rows(rows)) * 8;
+  auto free_cols = [&] {
+    for (int64_t* p : cols) hawk_b200_free(ctx_, p);
+  };
+  try {
+    for (const AttributeSpec& a : schema) {
+      void* p = nullptr;
+      check(hawk_b200_alloc(ctx_, bytes, &p), "column allocation");
+      cols.push_back(static_cast<int64_t*>(p));
+      check(hawk_b200_memset(ctx_, p, 0, bytes), "column padding");
+      kinds.push_back(static_cast<int32_t>(a.kind));
+    }
+  } catch (...) {
+    free_cols();
+    throw;
+  }
+  int64_t bad_record = -1;
+  int32_t bad_field = -1;
+  const int32_t st = hawk_b200_csv_parse(csv, static_cast<int32_t>(schema.size()), kinds.data(), cols.data(),
+                                         &bad_record, &bad_field);
+  if (st == HAWK_ERR_UNSUPPORTED || st == HAWK_ERR_INVALID_PARAMS) {
+    free_cols();
+    put_table(std::make_shared<Table>(hawk::load_csv(path, name, schema, options)));
+    return;
+  }
+  if (st != HAWK_OK) {
+    free_cols();
+    check(st, "CSV parse");
+  }
+  std::vector<std::vector<std::string>> lexicons(schema.size());
+  for (std::size_t c = 0; c < schema.size(); ++c) {
+    DeviceColumn d;
+    d.name = schema[c].name;
+    d.kind = schema[c].kind;
+    d.d_data = cols[c];
+    if (schema[c].kind == ColumnKind::String) {
+      const int64_t n = hawk_b200_csv_lexicon_size(csv, static_cast<int32_t>(c));
+      for (int64_t i = 0; i < n; ++i) lexicons[c].emplace_back(hawk_b200_csv_lexicon(csv, static_cast<int32_t>(c), i));
+      d.distinct = n;
+    }
+    dt.columns.push_back(d);
+  }
+  dt.catalog = make_catalog_stub(name, schema, lexicons);
+  check(hawk_b200_ctx_synchronize(ctx_), "CSV ingest");
+  impl_->tables[name] = std::move(dt);
+}
+
 void Engine::drop_table(const std::string& name) {
   ++generation_;
   auto it = impl_->tables.find(name);
@@ -466,17 +546,6 @@ struct TerminalState {
   std::vector<int64_t> host;  // copied device results
 };
 
-Value decode_value(const PipelineSet& set, const OutputColumn& oc, int64_t raw) {
-  switch (oc.kind) {
-    case ColumnKind::Int64: return raw;
-    case ColumnKind::Float64: return bits_to_double(raw);
-    case ColumnKind::String: {
-      const Table& lt = *set.tables.at(static_cast<std::size_t>(oc.lexicon_table));
-      return lt.column(static_cast<std::size_t>(oc.lexicon_column)).decode(raw);
-    }
-  }
-  return raw;
-}
 
 // A persistent pool of host threads for large results (TPC-H Q3 SF100
 // returns 1.2M groups): spawning threads per call cost more than the copy.

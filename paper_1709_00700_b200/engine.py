@@ -75,14 +75,22 @@ class TypeError_(HawkError):
     code = 13
 
 
+class ParseError_(HawkError):
+    code = 14
+
+
+class IoError_(HawkError):
+    code = 15
+
+
 _BY_CODE = {c.code: c for c in (UnsupportedPlan, InvalidConfig, Unsupported, PlanTooLarge,
                                 CapacityExceeded, DuplicateKey, EmptyAggregate, DivergentPlan,
                                 InvalidParams, SyntaxError_, UnknownTable, UnknownAttribute,
-                                TypeError_)}
+                                TypeError_, ParseError_, IoError_)}
 ERROR_NAMES = {1: "UnsupportedPlan", 2: "InvalidConfig", 3: "Unsupported", 4: "PlanTooLarge",
                5: "CapacityExceeded", 6: "DuplicateKey", 7: "EmptyAggregate",
                8: "DivergentPlan", 9: "InvalidParams", 10: "SyntaxError", 11: "UnknownTable",
-               12: "UnknownAttribute", 13: "TypeError"}
+               12: "UnknownAttribute", 13: "TypeError", 14: "ParseError", 15: "IoError"}
 
 
 def _raise(status: int):
@@ -253,6 +261,16 @@ class Engine:
     def generate(self, table: int, sf: float, seed: int = 42, row_begin: int = 0, rows: int = -1):
         """Generates a synthetic table (include/hawk_gen.h) directly in HBM."""
         _check(self._lib.hawk_engine_generate(self._h, table, sf, seed, row_begin, rows))
+
+    def load_csv(self, path: str, name: str, schema: list[tuple[str, int]], delimiter: str = ",",
+                 header: bool = False):
+        """A CSV file into device columns, parsed on the device with the
+        reference's load_csv rules (storage_csv.cpp:111-155). schema: (column,
+        kind) pairs, kind INT64 / FLOAT64 / STRING."""
+        names = (C.c_char_p * len(schema))(*[n.encode() for n, _ in schema])
+        kinds = (C.c_int32 * len(schema))(*[k for _, k in schema])
+        _check(self._lib.hawk_engine_load_csv(self._h, path.encode(), name.encode(), len(schema), names,
+                                              kinds, delimiter.encode(), int(header)))
 
     def drop(self, name: str):
         _check(self._lib.hawk_engine_drop(self._h, name.encode()))

@@ -35,6 +35,7 @@ def ora():
         _sig(lib, "ora_table_new", vp, cp, i32, C.POINTER(cp), C.POINTER(i32), i64, C.POINTER(vp),
              C.POINTER(C.POINTER(cp)), C.POINTER(i64), cp, i32)
         _sig(lib, "ora_table_gen", vp, cp, i64, u64, cp, i32)
+        _sig(lib, "ora_table_load_csv", vp, cp, cp, i32, C.POINTER(cp), C.POINTER(i32), C.c_char, i32, cp, i32)
         _sig(lib, "ora_table_free", None, vp)
         _sig(lib, "ora_table_rows", i64, vp)
         _sig(lib, "ora_table_ncols", i32, vp)
@@ -118,6 +119,19 @@ class OraTable:
     def generated(cls, which: str, n: int, seed: int) -> "OraTable":
         err = C.create_string_buffer(512)
         h = ora().ora_table_gen(which.encode(), n, seed, err, 512)
+        if not h:
+            raise RuntimeError(err.value.decode())
+        return cls(h)
+
+    @classmethod
+    def load_csv(cls, path: str, name: str, schema, delimiter: str = ",", header: bool = False) -> "OraTable":
+        """The reference's own load_csv (storage_csv.cpp:111-155); raises
+        RuntimeError with the reference's ParseError / IoError message."""
+        names = (cp * len(schema))(*[n.encode() for n, _ in schema])
+        kinds = (i32 * len(schema))(*[k for _, k in schema])
+        err = C.create_string_buffer(1024)
+        h = ora().ora_table_load_csv(path.encode(), name.encode(), len(schema), names, kinds,
+                                     delimiter.encode(), int(header), err, 1024)
         if not h:
             raise RuntimeError(err.value.decode())
         return cls(h)
