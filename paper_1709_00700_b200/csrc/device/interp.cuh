@@ -150,7 +150,11 @@ __device__ __forceinline__ void load_column(const KParams& kp, int slot, const B
 #pragma unroll
     for (int j = 0; j < R; ++j) v[j] = ((b.valid >> j) & 1u) ? ldg64_stream(c + b.row(j)) : 0ull;
   } else if constexpr (ACCESS == HAWK_COALESCED) {
+#ifdef HK_NO_STAGE  // compiled programs that never stage: no shared-memory tile path
+    if (false) {
+#else
     if (b.stage) {  // staged tile in shared memory (128-bit LDS per row pair)
+#endif
       const int64_t* t = b.stage + (size_t)kp.stage_of[slot] * b.B * R;
 #pragma unroll
       for (int j = 0; j < R; j += 2) {

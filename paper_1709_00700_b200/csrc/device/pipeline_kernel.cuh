@@ -296,6 +296,54 @@ __device__ __forceinline__ void hagg_static(const KParams& kp, const Batch<R, AC
     off[j] = tw[j] >> 1;
   }
   const uint32_t local_base = smem_addr(local_table);
+  if constexpr (ROLE == K_HAGG_LOCAL) {
+    // Fast path: every live row of the batch has thread-private accumulators
+    // (TPC-H Q1 after each CTA's first rows). Branch-free: rows that are not
+    // live add the aggregate's identity to a live row's accumulators, and the
+    // loop runs rows outermost, so each row reads all of its A accumulators
+    // before writing any: the shared-memory read-modify-writes of one row
+    // overlap instead of forming one chain through every (aggregate, row).
+    uint32_t live = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) live |= (uint32_t)(tw[j] != 0ull) << j;
+    if (GP > 0 && live != 0u && pmask == live) {
+      const int first = __ffs(live) - 1;
+      u64 any_off = off[0];
+#pragma unroll
+      for (int j = R - 1; j >= 0; --j)
+        if (j == first) any_off = off[j];
+      u64 av[A][R];
+      StaticFor<0, A>::run([&](auto ac) {
+        constexpr int a = decltype(ac)::value;
+        constexpr int fn = P::kAggFn[a], ty = P::kAggType[a];
+        if constexpr (fn == HAWK_COUNT) {
+#pragma unroll
+          for (int j = 0; j < R; ++j) av[a][j] = (live >> j) & 1u;
+        } else {
+          P::template agg_value<a, ACCESS, PRED, R>(kp, b, s, vals, av[a]);
+          const u64 id = agg_identity(fn, ty);
+#pragma unroll
+          for (int j = 0; j < R; ++j) av[a][j] = ((live >> j) & 1u) ? av[a][j] : id;
+        }
+      });
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        u64* base = priv + (((live >> j) & 1u) ? off[j] : any_off);
+        u64 acc[A];
+#pragma unroll
+        for (int a = 0; a < A; ++a) acc[a] = base[(size_t)a * B];
+        StaticFor<0, A>::run([&](auto ac) {
+          constexpr int a = decltype(ac)::value;
+          constexpr int fn = P::kAggFn[a], ty = P::kAggType[a];
+          if constexpr (fn == HAWK_COUNT || (fn == HAWK_SUM && ty == HAWK_I64)) acc[a] += av[a][j];
+          else acc[a] = agg_combine(fn, ty, acc[a], av[a][j]);
+        });
+#pragma unroll
+        for (int a = 0; a < A; ++a) base[(size_t)a * B] = acc[a];
+      }
+      return;
+    }
+  }
   StaticFor<0, A>::run([&](auto ac) {
     constexpr int a = decltype(ac)::value;
     constexpr int fn = P::kAggFn[a], ty = P::kAggType[a];

@@ -26,6 +26,25 @@ def test_b200_library_exports_cross_header():
     assert hasattr(lib, names[0])
 
 
+def test_b200_library_exports_comm_and_csv_headers():
+    lib = _native.b200()
+    for header, expect in (("hawk_b200_comm.h", 11), ("hawk_b200_csv.h", 8)):
+        names = _native.declared_symbols(os.path.join(ROOT, "include", header))
+        assert len(names) == expect, (header, names)
+        missing = [n for n in names if not hasattr(lib, n)]
+        assert not missing, (header, missing)
+
+
+def test_every_header_is_covered():
+    # every public header's declarations are exported by one of the libraries
+    libs = [_native.b200(), _native.engine()]
+    for h in sorted(os.listdir(os.path.join(ROOT, "include"))):
+        if not h.endswith(".h") or h == "hawk_gen.h":  # hawk_gen.h is header-only (inline)
+            continue
+        for n in _native.declared_symbols(os.path.join(ROOT, "include", h)):
+            assert any(hasattr(lib, n) for lib in libs), (h, n)
+
+
 def test_engine_library_exports_header():
     lib = _native.engine()
     names = _native.declared_symbols(os.path.join(ROOT, "include", "hawk_b200_engine.h"))
