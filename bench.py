@@ -32,17 +32,30 @@ sys.path.insert(0, ROOT)
 
 METRIC = "input tuples/sec & HBM GB/s (roofline frac) per TPC-H/SSB query, 1/2/4/8 B200"
 
-# learned/selected variant per query (--config overrides)
+# the variant per query: the configuration Algorithm 1 learned on a B200
+# (tools/learn_all.py -> paper_1709_00700_b200/learned/<query>.conf); these
+# literals are only the fallback when no learned file exists (--config overrides)
 DEFAULT_CONFIG = {
     "tpch_q6": "single_pass/sequential/branched/u=2;global_hash/sequential/branched/linear_probing/multiply_shift/wg=256/u=2",
     "tpch_q1": "single_pass/coalesced/branched;local_hash/coalesced/predicated/linear_probing/murmur/wg=256/ht=8",
     "ssb_q11": "single_pass/coalesced/branched/u=4;global_hash/coalesced/branched/linear_probing/multiply_shift/wg=64",
-    "ssb_q41": "single_pass/coalesced/branched;global_hash/coalesced/branched/linear_probing/multiply_shift/wg=256",
+    "ssb_q41": "single_pass/coalesced/branched;local_hash/coalesced/branched/linear_probing/multiply_shift/wg=256/ht=8",
     "tpch_q3": "single_pass/coalesced/branched/u=4;global_hash/coalesced/branched/linear_probing/multiply_shift/wg=64",
 }
 # BASELINE.json configs: the scale factor each query is quoted at
 BASELINE_SF = {"tpch_q6": 1.0, "tpch_q1": 10.0, "ssb_q11": 10.0, "ssb_q41": 100.0, "tpch_q3": 100.0}
 DEFAULT_SF = BASELINE_SF
+
+
+def default_config(query: str) -> str:
+    """The learned configuration of `query` (key-value file), else the fallback."""
+    path = os.path.join(ROOT, "paper_1709_00700_b200", "learned", f"{query}.conf")
+    if os.path.exists(path):
+        from paper_1709_00700_b200.engine import load_config
+        return load_config(path)
+    return DEFAULT_CONFIG[query]
+
+
 WORKLOAD_NAME = {"tpch_q6": "TPC-H Q6", "tpch_q1": "TPC-H Q1", "ssb_q11": "SSB Q1.1",
                  "ssb_q41": "SSB Q4.1", "tpch_q3": "TPC-H Q3"}
 
@@ -270,7 +283,7 @@ def query_bytes(engine, query: str, sf: float, per_rank: int, world: int, result
         big["customer_probes"] = cap(dg.table_rows(dg.CUSTOMER, sf * world)) * 16 > l2
         big["group_updates"] = True
         for k, sql in ACCOUNTING[query].items():
-            n = int(engine.run(sql, DEFAULT_CONFIG[query]).columns[0].values[0])
+            n = int(engine.run(sql, default_config(query)).columns[0].values[0])
             detail[k] = n * 32 if big[k] else 0
             total += detail[k]
     return {"terminal": fact_bytes, "whole_query": total, "detail": detail}
@@ -472,7 +485,7 @@ def main():
 
     query = args.query
     sf = args.sf or DEFAULT_SF[query]
-    cfg = args.config or DEFAULT_CONFIG[query]
+    cfg = args.config or default_config(query)
     sql = Q.BENCH[query][0]
     engine = Engine(local)
     apply_options(engine, args)
@@ -570,12 +583,21 @@ def main():
                       f"({ref.shards} shards), merged; 1 run",
             "cpu_model": info["cpu_model"], "host_cores": info["cores"]}
         del ref
+        # the reference's CPU variant (cpu-o), restated in
+        # oracle/cpu_o.cpp over the reference's own pipeline programs
+        from ref_sharded import cpu_variant_rate
+        rate, threads, rows = cpu_variant_rate(query, sf, args.seed)
+        line["cpu_variant"] = {
+            "value": rate, "unit": "tuples/s", "cores": threads, "kind": "port",
+            "sample": f"cpu-o variant (single-pass, local hash, sequential, linear probing, murmur, branched, "
+                      f"one worker per host thread) over all {rows} fact rows of {WORKLOAD_NAME[query]} "
+                      f"SF{sf:g}; 1 run after 1 warm-up"}
     if world == 1 and not args.no_per_query and args.config is None and args.sf is None:
         drop_tables(engine, query)
         line["per_query"] = {}
         for q in DEFAULT_CONFIG:
             try:
-                line["per_query"][q] = measure_query(engine, stream, q, BASELINE_SF[q], DEFAULT_CONFIG[q],
+                line["per_query"][q] = measure_query(engine, stream, q, BASELINE_SF[q], default_config(q),
                                                      args.per_query_steps, 3, l2, peak)
             except Exception as e:  # noqa: BLE001 - reported in the line
                 line["per_query"][q] = {"error": f"{type(e).__name__}: {e}"}

@@ -29,6 +29,10 @@
 #include "hawk/storage/csv.hpp"
 #include "hawk/storage/generator.hpp"
 
+namespace hawk::cpu_o {
+Table execute(const std::string& sql, const std::vector<TablePtr>& tables, int threads);
+}
+
 namespace {
 
 struct OraTable {
@@ -182,6 +186,20 @@ OraTable* ora_execute(OraDb* db, const char* sql, int* err_class, char* err, int
   try {
     auto plan = hawk::sql::parse_query(sql, hawk::sql::make_catalog(db->tables));
     hawk::Table out = hawk::reference_execute(plan, db->tables);
+    *err_class = 0;
+    return new OraTable{std::make_shared<hawk::Table>(std::move(out))};
+  } catch (const std::exception& e) {
+    *err_class = classify(e);
+    put_err(err, errlen, e.what());
+    return nullptr;
+  }
+}
+
+// The reference's CPU variant "cpu-o" over the reference pipeline programs
+// (oracle/cpu_o.cpp); same error convention as ora_execute.
+OraTable* ora_execute_cpu_o(OraDb* db, const char* sql, int threads, int* err_class, char* err, int errlen) {
+  try {
+    hawk::Table out = hawk::cpu_o::execute(sql, db->tables, threads);
     *err_class = 0;
     return new OraTable{std::make_shared<hawk::Table>(std::move(out))};
   } catch (const std::exception& e) {

@@ -365,7 +365,12 @@ int32_t prepare(hawk_ctx* ctx, const hawk_pipeline& pipe, const hawk_variant& v,
   kp.split = ctx->jit && ctx->compact && split_rows_for(pipe, v, role);
   kp.split_drain = !kp.split ? 1 : ctx->drain_rows > 0 ? ctx->drain_rows : auto_drain(pipe);
   kp.split_bits = kp.split ? ctx->split_bits : 0;
-  kp.min_ctas = ctx->min_ctas;
+  // thread-private group-by accumulators (scan + group-by, TPC-H Q1) take
+  // more registers than 3 CTAs/SM leave; 2 CTAs of 256 threads measured
+  // 0.67 vs 0.79 ms on Q1 SF10 (profiles/ab_r02_q1_min_ctas.txt)
+  const bool priv = role == hk::K_HAGG_LOCAL && pipe.naggs > 0 &&
+                    (ctx->priv_groups >= 0 ? ctx->priv_groups > 0 : pipe.nprobe == 0);
+  kp.min_ctas = ctx->min_ctas > 0 ? ctx->min_ctas : (priv && ctx->jit ? 2 : 0);
   shape.jit_fn = nullptr;
   if (ctx->jit) {  // compiled program: generate + NVRTC (cached), see jit.cu
     std::string err;

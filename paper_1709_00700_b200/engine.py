@@ -129,18 +129,39 @@ class Partial(NamedTuple):
     launches: int
 
 
-@dataclass
 class Result:
-    columns: list[Column]
-    kernel_ms: float
-    wall_ms: float
-    input_tuples: int
-    launches: int
-    pipelines: list[dict] = field(default_factory=list)
+    """A query result. Columns are zero-copy views of the engine's result
+    buffers, built on first access (as are the per-pipeline metrics), so a
+    caller that only reads timings pays no per-column work."""
+
+    def __init__(self, owner, lib, r):
+        self._owner, self._lib, self._r = owner, lib, r
+        self.kernel_ms = lib.hawk_result_kernel_ms(r)
+        self.wall_ms = lib.hawk_result_wall_ms(r)
+        self.input_tuples = lib.hawk_result_input_tuples(r)
+        self.launches = lib.hawk_result_launches(r)
+        self.rows = lib.hawk_result_rows(r)
+        self._columns = None
+        self._pipelines = None
 
     @property
-    def rows(self) -> int:
-        return len(self.columns[0].values) if self.columns else 0
+    def columns(self) -> list[Column]:
+        if self._columns is None:
+            self._columns = _columns_of(self._lib, self._r, self._owner, self.rows)
+        return self._columns
+
+    @property
+    def pipelines(self) -> list[dict]:
+        if self._pipelines is None:
+            pipes = []
+            for line in self._lib.hawk_result_metrics_text(self._r).decode().splitlines():
+                p = line.split()
+                if len(p) >= 8:
+                    pipes.append(dict(variant=p[0], kernel_ms=float(p[1]), launches=int(p[2]),
+                                      rows_in=int(p[3]), rows_out=int(p[4]), grid=int(p[5]),
+                                      block=int(p[6]), retries=int(p[7])))
+            self._pipelines = pipes
+        return self._pipelines
 
     def column(self, name: str) -> Column:
         for c in self.columns:
@@ -162,13 +183,8 @@ class _ResultOwner:
             pass
 
 
-def _result_from(lib, r) -> Result:
-    """Result columns are zero-copy views of the engine's result buffers; the
-    hawk_result lives as long as any of them (large results, e.g. TPC-H Q3
-    SF100's 1.2M groups, are not copied again)."""
+def _columns_of(lib, r, owner, n) -> list[Column]:
     cols = []
-    owner = _ResultOwner(lib, r)
-    n = lib.hawk_result_rows(r)
     for c in range(lib.hawk_result_ncols(r)):
         kind = lib.hawk_result_col_kind(r, c)
         name = lib.hawk_result_col_name(r, c).decode()
@@ -185,15 +201,14 @@ def _result_from(lib, r) -> Result:
             lex = [lib.hawk_result_col_lexicon(r, c, i).decode()
                    for i in range(lib.hawk_result_col_lexicon_size(r, c))]
         cols.append(Column(name, kind, vals, lex))
-    pipes = []
-    for line in lib.hawk_result_metrics_text(r).decode().splitlines():
-        p = line.split()
-        if len(p) >= 8:
-            pipes.append(dict(variant=p[0], kernel_ms=float(p[1]), launches=int(p[2]),
-                              rows_in=int(p[3]), rows_out=int(p[4]), grid=int(p[5]),
-                              block=int(p[6]), retries=int(p[7])))
-    return Result(cols, lib.hawk_result_kernel_ms(r), lib.hawk_result_wall_ms(r),
-                  lib.hawk_result_input_tuples(r), lib.hawk_result_launches(r), pipes)
+    return cols
+
+
+def _result_from(lib, r) -> Result:
+    """Result columns are zero-copy views of the engine's result buffers; the
+    hawk_result lives as long as the Result or any of its column arrays
+    (large results, e.g. TPC-H Q3 SF100's 1.2M groups, are not copied again)."""
+    return Result(_ResultOwner(lib, r), lib, r)
 
 
 class Engine:

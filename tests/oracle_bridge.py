@@ -53,6 +53,7 @@ def ora():
         _sig(lib, "ora_db_add", None, vp, vp)
         _sig(lib, "ora_execute", vp, vp, cp, C.POINTER(i32), cp, i32)
         _sig(lib, "ora_pipeline_count", i32, vp, cp, cp, i32)
+        _sig(lib, "ora_execute_cpu_o", vp, vp, cp, i32, C.POINTER(i32), cp, i32)
         _ora = lib
     return _ora
 
@@ -200,6 +201,16 @@ class OraDb:
         cls = i32()
         err = C.create_string_buffer(1024)
         h = ora().ora_execute(self.h, sql.encode(), C.byref(cls), err, 1024)
+        if not h:
+            raise OraError(cls.value, err.value.decode())
+        return OraTable(h)
+
+    def execute_cpu_o(self, sql: str, threads: int = 0) -> OraTable:
+        """The reference's CPU variant (cpu-o, oracle/cpu_o.cpp) on `threads`
+        host threads (0 = all)."""
+        cls = i32()
+        err = C.create_string_buffer(1024)
+        h = ora().ora_execute_cpu_o(self.h, sql.encode(), threads or (os.cpu_count() or 1), C.byref(cls), err, 1024)
         if not h:
             raise OraError(cls.value, err.value.decode())
         return OraTable(h)

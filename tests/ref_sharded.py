@@ -151,3 +151,20 @@ def cpu_model() -> str:
     except OSError:
         pass
     return "unknown"
+
+
+def cpu_variant_rate(query: str, sf: float, seed: int = 42, threads: int | None = None):
+    """The reference's CPU variant (cpu-o, oracle/cpu_o.cpp) over the whole
+    workload on every host thread: (fact tuples/s, threads, fact rows)."""
+    threads = threads or os.cpu_count() or 1
+    _, tables, fact = Q.BENCH[query]
+    db = OraDb()
+    for t in tables:
+        db.add(_table(t, sf, seed, 0, dg.table_rows(t, sf), _referenced(query, t), threads))
+    sql = Q.BENCH[query][0]
+    db.execute_cpu_o(sql, threads)
+    t0 = time.perf_counter()
+    db.execute_cpu_o(sql, threads)
+    dt = time.perf_counter() - t0
+    n = dg.table_rows(fact, sf)
+    return n / dt, threads, n

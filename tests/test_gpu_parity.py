@@ -438,7 +438,7 @@ def test_sf10_bench_queries_match_port(key):
         for t in tables:
             e.generate(t, 10.0, 42)
         expected = port_rows(key, 10.0, 42, threads=os.cpu_count() or 8)
-        for cfg in (bench.DEFAULT_CONFIG[key], CONFIGS[1]):
+        for cfg in (bench.default_config(key), CONFIGS[1]):
             got = e.run(sql, cfg)
             rows = sorted(zip(*[c.values.tolist() for c in got.columns]))
             assert len(rows) == len(expected), (key, cfg)
@@ -470,7 +470,7 @@ def test_sf100_bench_queries_match_port(key):
         for t in tables:
             e.generate(t, 100.0, 42)
         expected = port_rows(key, 100.0, 42, threads=os.cpu_count() or 8)
-        for cfg in [bench.DEFAULT_CONFIG[key]] + SF100_CONFIGS:
+        for cfg in [bench.default_config(key)] + SF100_CONFIGS:
             got = e.run(sql, cfg)
             rows = sorted(zip(*[c.values.tolist() for c in got.columns]))
             assert len(rows) == len(expected), (key, cfg, len(rows), len(expected))

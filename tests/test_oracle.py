@@ -164,3 +164,31 @@ def test_cross_join_oracle_closed_form():
     assert [c.name for c in cols] == ["n", "s"]
     assert int(cols[0].values[0]) == int((q < 10).sum()) * int((a_w < 5).sum())
     assert int(cols[1].values[0]) == int(q[q < 10].sum()) * int(a_w[a_w < 5].sum())
+
+
+@pytest.mark.parametrize("key", [k for k, _ in harness.BENCH])
+def test_cpu_o_variant_matches_reference_execute(key):
+    # the reference's CPU variant (cpu-o; oracle/cpu_o.cpp)
+    # equals reference_execute on every BASELINE query and thread count
+    db_name = "ssb" if key.startswith("ssb") else "tpch"
+    db = harness.oracle_db(harness.bench_tables(db_name, 0.02, 42))
+    sql = dict(harness.BENCH)[key]
+    ref = db.execute(sql)
+    for threads in (1, 8):
+        got = db.execute_cpu_o(sql, threads)
+        assert ref.compare(got) is None, (key, threads)
+
+
+def test_cpu_o_variant_micro_semantics():
+    from oracle_bridge import OraError
+    db = harness.oracle_db(harness.micro_tables(20000, 5))
+    sqls = [s for _, s in harness.MICRO] + [
+        "select lo_quantity, sum(lo_revenue / (lo_discount - 5)), min(lo_extendedprice * 0.5), "
+        "max(lo_discount), avg(lo_revenue) from lineorder group by lo_quantity",
+        "select count(*), sum(lo_quantity) from lineorder where lo_quantity > 100",
+    ]
+    for sql in sqls:
+        assert db.execute(sql).compare(db.execute_cpu_o(sql, 4)) is None, sql
+    with pytest.raises(OraError) as e:
+        db.execute_cpu_o("select min(lo_quantity) from lineorder where lo_quantity > 100", 4)
+    assert e.value.cls == 7

@@ -19,7 +19,7 @@ from paper_1709_00700_b200 import queries as Q  # noqa: E402
 def main():
     query, sf = sys.argv[1], float(sys.argv[2])
     sets = sys.argv[3:] or [""]
-    cfg = os.environ.get("AB_CONFIG") or bench.DEFAULT_CONFIG[query]
+    cfg = os.environ.get("AB_CONFIG") or bench.default_config(query)
     import torch
     e = Engine(0)
     e.set_option("jit", 1)
