@@ -274,7 +274,7 @@ def query_bytes(engine, query: str, sf: float, per_rank: int, world: int, result
     inserts = sum(p["rows_out"] for p in result.pipelines[:-1])
     detail["build_inserts"] = inserts * 16
     total += inserts * 16
-    if query in ACCOUNTING:
+    if query in ACCOUNTING and not os.environ.get("HAWK_BENCH_NO_ACCOUNTING"):
         big = {}
         # join tables are sized next_pow2(2 x build rows) x 16 B; the orders
         # table exceeds L2 at every SF >= 1, the customer table from SF ~60

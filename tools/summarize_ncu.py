@@ -29,8 +29,20 @@ METRICS = {
     "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio": "stall_short_scoreboard",
     "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio": "stall_wait",
     "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio": "stall_barrier",
+    "smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio": "stall_mio_throttle",
+    "lts__t_sectors_op_atom.sum": "l2_atomic_sectors",
+    "lts__t_sectors_op_red.sum": "l2_reduction_sectors",
+    "l1tex__t_set_accesses_pipe_lsu_mem_global_op_atom.sum": "global_atomic_requests",
+    "l1tex__t_set_accesses_pipe_lsu_mem_global_op_red.sum": "global_reduction_requests",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum": "shared_atomic_wavefronts",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum": "shared_wavefronts",
+    "launch__occupancy_limit_registers": "occupancy_limit_registers",
+    "launch__occupancy_limit_shared_mem": "occupancy_limit_smem",
+    "sm__maximum_warps_per_active_cycle_pct": "theoretical_occupancy_pct",
 }
-summary, traffic = {}, {}
+summary = {}
+traffic_path = os.path.join(dst, "ncu_traffic.json")
+traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
 for rep in sorted(glob.glob(os.path.join(src, "full_*.ncu-rep"))):
     q = os.path.basename(rep)[len("full_"):-len(".ncu-rep")]
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
