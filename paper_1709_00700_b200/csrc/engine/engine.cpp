@@ -119,6 +119,22 @@ struct Engine::Impl {
   // inside a cached PipelineSet): sizes the aggregation table and the
   // speculative read-back of the next run
   std::unordered_map<std::string, int64_t> group_hint;
+  // key of a lowered program on its driver table: the op arrays' bytes (no
+  // padding in these PODs), counts, and the driver's identity and size
+  static std::string program_key(const hawk_pipeline& p, const DeviceTable& driver) {
+    std::string k = driver.name;
+    auto put = [&](const void* d, size_t n) { k.append(static_cast<const char*>(d), n); };
+    const int64_t sizes[] = {driver.rows, driver.row_offset, p.sink, p.nfilter, p.nprobe, p.npost,
+                             p.narith, p.nkeys, p.naggs, p.nproject};
+    put(sizes, sizeof sizes);
+    put(p.filter, sizeof(hawk_compare) * static_cast<size_t>(p.nfilter));
+    put(p.probe, sizeof(hawk_probe) * static_cast<size_t>(p.nprobe));
+    put(p.post, sizeof(hawk_compare) * static_cast<size_t>(p.npost));
+    put(p.arith, sizeof(hawk_arith) * static_cast<size_t>(p.narith));
+    put(p.keys, sizeof(hawk_operand) * static_cast<size_t>(p.nkeys));
+    put(p.aggs, sizeof(hawk_agg) * static_cast<size_t>(p.naggs));
+    return k;
+  }
 
   void* acquire(size_t bytes) {
     auto it = pool.lower_bound(bytes);
@@ -1187,8 +1203,7 @@ static QueryRun run_query(Engine& e, Engine::Impl& I, const PipelineSet& set,
     const bool grouped = lp.pipe.sink == HAWK_SINK_HASH_AGGREGATE;
     // keyed by the lowered program and its driver table (plan objects are
     // recycled, their addresses are no key)
-    const std::string hint_key = driver.name + "#" + std::to_string(driver.rows) + "#" +
-                                 std::to_string(driver.row_offset) + "\n" + describe(lp.pipe);
+    const std::string hint_key = Engine::Impl::program_key(lp.pipe, driver);
     auto hint_it = I.group_hint.find(hint_key);
     const int64_t hint = hint_it == I.group_hint.end() ? -1 : hint_it->second;
     int64_t bound = grouped ? I.groups_bound(lp, set, driver.rows) : 0;
