@@ -192,3 +192,38 @@ def test_cpu_o_variant_micro_semantics():
     with pytest.raises(OraError) as e:
         db.execute_cpu_o("select min(lo_quantity) from lineorder where lo_quantity > 100", 4)
     assert e.value.cls == 7
+
+
+@pytest.mark.parametrize("key", [k for k, _ in harness.BENCH])
+def test_port_matches_reference_execute_sf1(key):
+    # the restatement pinned against reference_execute at SF1
+    # (reference_execute itself, one run over the whole SF1 tables)
+    db_name = "ssb" if key.startswith("ssb") else "tpch"
+    db = harness.oracle_db(harness.bench_tables(db_name, 1.0, 42))
+    ref = db.execute(dict(harness.BENCH)[key]).canonical_rows()
+    ours = port_rows(key, 1.0, 42, threads=os.cpu_count() or 4)
+    assert len(ref) == len(ours)
+    for a, b in zip(ref, ours):
+        for x, y in zip(a, b):
+            assert abs(x - y) <= 1e-9 * max(1.0, abs(x), abs(y)) if isinstance(x, float) else x == y
+
+
+@pytest.mark.skipif(not os.environ.get("HAWK_SLOW"), reason="SF10 pin: set HAWK_SLOW=1 (~20 GB host RAM)")
+@pytest.mark.parametrize("key", [k for k, _ in harness.BENCH])
+def test_port_matches_reference_execute_sf10(key):
+    # SF10: reference_execute over row shards of the fact table on every core
+    # (tests/ref_sharded.py, shard results merged), against the streaming port
+    from ref_sharded import ShardedReference
+    ref = ShardedReference(key, 10.0, 42).run()
+    rows = []
+    for r in ref:
+        v = [int(x) for x in r]
+        if key == "tpch_q1":
+            v = v[:6] + [_f64(x) for x in v[6:9]] + v[9:]
+        rows.append(tuple(v))
+    rows.sort()
+    ours = port_rows(key, 10.0, 42, threads=os.cpu_count() or 4)
+    assert len(rows) == len(ours)
+    for a, b in zip(rows, ours):
+        for x, y in zip(a, b):
+            assert abs(x - y) <= 1e-9 * max(1.0, abs(x), abs(y)) if isinstance(x, float) else x == y
