@@ -252,7 +252,8 @@ typedef struct hawk_output {
 enum {
   HAWK_FLAG_DUPLICATE = 1,   /* HASH_PUT saw a key twice (planner_reference.cpp:171-174) */
   HAWK_FLAG_CUCKOO_FAIL = 2, /* eviction chain exceeded 32 */
-  HAWK_FLAG_TABLE_FULL = 4   /* aggregation table overflow */
+  HAWK_FLAG_TABLE_FULL = 4,  /* aggregation table overflow */
+  HAWK_FLAG_CHECK = 8        /* a device bounds check failed (option "checked") */
 };
 
 typedef struct hawk_ctx hawk_ctx;
@@ -280,7 +281,9 @@ int32_t hawk_b200_ctx_synchronize(hawk_ctx* ctx);
  * "dense_keys" (HASH_AGGREGATE: use hawk_pipeline.dense_groups; default 1),
  * "compact" (compiled, branched: compact live rows after the first probe; default 1),
  * "min_ctas" (compiled: __launch_bounds__ minimum CTAs per SM; 0 = by unroll),
- * "priv_groups" (HASH_AGGREGATE local: groups with thread-private accumulators). */
+ * "priv_groups" (HASH_AGGREGATE local: groups with thread-private accumulators),
+ * "checked" (compiled programs carry device-side bounds checks on every
+ * indexed access; a failure raises HAWK_FLAG_CHECK). */
 int32_t hawk_b200_ctx_set_option(hawk_ctx* ctx, const char* name, int64_t value);
 /* Reads an option back ("dense_join": 1 = join builds over a dense key range
  * use a direct-addressed index instead of the variant's hash table; default 1). */

@@ -36,6 +36,7 @@ struct hawk_ctx {
   int dense_join = 1;       // engine: dense-key join builds use a direct-addressed index
   int drain_rows = 0;       // compiled, compacted: queued rows per lane per drain (0 = auto)
   int split_bits = 1;       // compiled, compacted: key bitmaps for the first (1) / every (2) probe
+  int checked = 0;          // compiled programs with device bounds checks
   // COALESCED: stage pass tiles in smem with TMA. Off by default since the
   // private-accumulator group-by: TPC-H Q1 SF10 terminal 0.744 -> 0.712 ms
   // unstaged without the pass barrier, TPC-H Q6 unchanged (0.0343 ms both;
@@ -365,6 +366,7 @@ int32_t prepare(hawk_ctx* ctx, const hawk_pipeline& pipe, const hawk_variant& v,
   kp.split = ctx->jit && ctx->compact && split_rows_for(pipe, v, role);
   kp.split_drain = !kp.split ? 1 : ctx->drain_rows > 0 ? ctx->drain_rows : auto_drain(pipe);
   kp.split_bits = kp.split ? ctx->split_bits : 0;
+  kp.checked = ctx->checked;
   // thread-private group-by accumulators (scan + group-by, TPC-H Q1) take
   // more registers than 3 CTAs/SM leave; 2 CTAs of 256 threads measured
   // 0.67 vs 0.79 ms on Q1 SF10 (profiles/ab_r02_q1_min_ctas.txt)
@@ -545,6 +547,10 @@ static void program_params(const hawk_pipeline& p, const hawk_variant& v, hk::KP
   kp.p = p;
   kp.split = split_rows_for(p, v, main_role(p, v));  // the default context options
   kp.split_drain = kp.split ? auto_drain(p) : 1;
+  // as prepare() with the default options: private-accumulator group-bys run 2 CTAs/SM
+  const int role = main_role(p, v);
+  kp.min_ctas = role == hk::K_HAGG_LOCAL && p.naggs > 0 && p.nprobe == 0 ? 2 : 0;
+  kp.checked = std::getenv("HAWK_CHECKED") != nullptr;  // compile-check the instrumented programs
   kp.split_bits = kp.split ? 1 : 0;
   kp.npre = compile_filters(p.filter, p.nfilter, kp.pre);
   kp.npost = compile_filters(p.post, p.npost, kp.post);
@@ -623,6 +629,10 @@ int32_t hawk_b200_ctx_set_option(hawk_ctx* ctx, const char* name, int64_t value)
     ctx->dense_join = value != 0;
     return HAWK_OK;
   }
+  if (std::strcmp(name, "checked") == 0) {
+    ctx->checked = value != 0;
+    return HAWK_OK;
+  }
   if (std::strcmp(name, "split_bits") == 0) {
     ctx->split_bits = (int)std::max<int64_t>(0, std::min<int64_t>(value, 2));
     return HAWK_OK;
@@ -641,7 +651,8 @@ int32_t hawk_b200_ctx_get_option(hawk_ctx* ctx, const char* name, int64_t* value
       {"min_ctas", ctx->min_ctas}, {"compact", ctx->compact}, {"dense_keys", ctx->dense_keys},
       {"stage_probes", ctx->stage_probes}, {"pass_sync", ctx->pass_sync}, {"jit", ctx->jit},
       {"stage", ctx->stage}, {"priv_groups", ctx->priv_groups}, {"dense_join", ctx->dense_join},
-      {"drain_rows", ctx->drain_rows}, {"split_bits", ctx->split_bits}};
+      {"drain_rows", ctx->drain_rows}, {"split_bits", ctx->split_bits},
+      {"checked", ctx->checked}};
   for (const auto& o : opts)
     if (std::strcmp(name, o.n) == 0) {
       *value = o.v;

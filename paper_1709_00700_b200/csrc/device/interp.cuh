@@ -91,10 +91,26 @@ struct KParams {
   int32_t smem_queue_off;             //   ... per-warp queues of (row, probe-0 row id)
   int32_t split_drain;                //   ... queued rows per lane per drain
   int32_t split_bits;                 //   ... key bitmaps for semi-join probes: 1 first, 2 all
+  int32_t checked;                    // compiled: device bounds checks (HK_CHECKED)
   int32_t smem_state_off;
   int32_t state_words;                // state words per thread
   int32_t rid_base, key_base, acc_base;
 };
+
+// Device-side bounds checks of the compiled programs' indexed accesses
+// (option "checked", -DHK_CHECKED): a failure raises HAWK_FLAG_CHECK and the
+// access is skipped. compute-sanitizer is unavailable on this pool; this is
+// the instrumented build that stands in for its memcheck.
+#ifdef HK_CHECKED
+#define HK_CHECK(kp, cond) \
+  do {                     \
+    if (!(cond)) atomicOr((kp).d_flags, HAWK_FLAG_CHECK); \
+  } while (0)
+#define HK_CHECKED_OK(kp, cond) ((cond) ? true : (atomicOr((kp).d_flags, HAWK_FLAG_CHECK), false))
+#else
+#define HK_CHECK(kp, cond) ((void)0)
+#define HK_CHECKED_OK(kp, cond) true
+#endif
 
 // R rows of one op pass.
 // COALESCED: the pass tile [base, base + B*R): thread t owns tile rows
@@ -146,6 +162,11 @@ template <int R, int ACCESS>
 __device__ __forceinline__ void load_column(const KParams& kp, int slot, const Batch<R, ACCESS>& b,
                                             u64 (&v)[R]) {
   const int64_t* __restrict__ c = reinterpret_cast<const int64_t*>(kp.p.d_columns[slot]);
+#ifdef HK_CHECKED
+#pragma unroll
+  for (int j = 0; j < R; ++j)  // rows inside the driver's padded extent
+    HK_CHECK(kp, !((b.valid >> j) & 1u) || (b.row(j) >= 0 && b.row(j) < kp.p.nrows + 64));
+#endif
   if constexpr (ACCESS == kGather) {  // compacted rows: gathers
 #pragma unroll
     for (int j = 0; j < R; ++j) v[j] = ((b.valid >> j) & 1u) ? ldg64_stream(c + b.row(j)) : 0ull;

@@ -235,6 +235,7 @@ __device__ __forceinline__ void hagg_static(const KParams& kp, const Batch<R, AC
             }
             if (in) {
               d = (int)idx;
+              HK_CHECK(kp, d < kp.p.dense_groups);
               // GP > 0: private accumulators are thread-owned and need no
               // ordering; GP == 0: the CTA slot's contents must be visible
               const int o = GP > 0 ? *reinterpret_cast<volatile int*>(dense_ord + d)
@@ -296,6 +297,13 @@ __device__ __forceinline__ void hagg_static(const KParams& kp, const Batch<R, AC
     off[j] = tw[j] >> 1;
   }
   const uint32_t local_base = smem_addr(local_table);
+#ifdef HK_CHECKED
+#pragma unroll
+  for (int j = 0; j < R; ++j) {  // private words and CTA-table slots inside their arrays
+    HK_CHECK(kp, !((pmask >> j) & 1u) || off[j] < (u64)GP * A * B);
+    HK_CHECK(kp, !((smask >> j) & 1u) || (tw[j] >> 2) < (u64)(1 << kp.local_log2) * (IMPL == HAWK_CUCKOO ? 2 : 1));
+  }
+#endif
   if constexpr (ROLE == K_HAGG_LOCAL) {
     // Fast path: every live row of the batch has thread-private accumulators
     // (TPC-H Q1 after each CTA's first rows). Branch-free: rows that are not
@@ -531,6 +539,7 @@ __device__ __forceinline__ void split_rows(const KParams& kp, const Batch<R, ACC
   const uint32_t total = __shfl_sync(mask, incl, last);
   if (total == 0u) return;
   uint32_t pos = qn + incl - c;
+  HK_CHECK(kp, qn + total <= (uint32_t)(32 * (R + D)));  // the warp's queue capacity
 #pragma unroll
   for (int j = 0; j < R; ++j)
     if ((alive >> j) & 1u) q[pos++] = make_uint2((uint32_t)(b.row(j) - cb), (uint32_t)vals.p0[j]);
@@ -872,7 +881,12 @@ __device__ __forceinline__ void pipeline_body(const KParams& kp) {
     // in flight; thread t consumes tile rows t + jB.
     const int64_t pass_rows = (int64_t)B * R;
     const int64_t npasses = (len + pass_rows - 1) / pass_rows;
+#ifdef HK_NO_STAGE  // compiled programs that never stage: no TMA tile pipeline at all
+    const int S = kp.prefetch_passes;
+    constexpr int C = 0;
+#else
     const int S = kp.prefetch_passes, C = kp.nprefetch;
+#endif
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kp.smem_stage_off);
     int64_t* stages = reinterpret_cast<int64_t*>(smem + kp.smem_stage_off + 128);
     if (threadIdx.x == 0 && C > 0) {

@@ -669,6 +669,12 @@ ResultColumns materialise(const PipelineSet& set, const PipelineProgram& prog,
   }
   ResultColumns out;
   out.rows = nrows;
+  out.columns.reserve(prog.output.size());
+  struct Plain {
+    int word;
+    int64_t* dst;
+  };
+  std::vector<Plain> plain;  // row-major words copied into int64 / float64 columns
   for (const OutputColumn& oc : prog.output) {
     ResultColumn col;
     col.name = oc.name;
@@ -698,21 +704,20 @@ ResultColumns materialise(const PipelineSet& set, const PipelineProgram& prog,
           col.floats[static_cast<std::size_t>(r)] = num / static_cast<double>(cnt);
         }
       });
-    } else if (oc.kind == ColumnKind::Float64) {
-      col.floats.resize(static_cast<std::size_t>(nrows));
-      parallel_rows(nrows, [&](int64_t b, int64_t e) {
-        for (int64_t r = b; r < e; ++r) col.floats[static_cast<std::size_t>(r)] = bits_to_double(at(r, word));
-      });
-    } else if (oc.kind == ColumnKind::Int64) {
-      col.ints.resize(static_cast<std::size_t>(nrows));
-      int64_t* dst = col.ints.data();
+    } else if (oc.kind == ColumnKind::Float64 || oc.kind == ColumnKind::Int64) {
+      // plain 8-byte words: copied together below in one pass over the rows
+      int64_t* dst;
+      if (oc.kind == ColumnKind::Float64) {
+        col.floats.resize(static_cast<std::size_t>(nrows));
+        dst = reinterpret_cast<int64_t*>(col.floats.data());
+      } else {
+        col.ints.resize(static_cast<std::size_t>(nrows));
+        dst = col.ints.data();
+      }
       if (column_major) {
         if (nrows > 0) std::memcpy(dst, rows + word * stride, static_cast<size_t>(nrows) * 8);
       } else {
-        const int64_t* src = rows + word;
-        parallel_rows(nrows, [&](int64_t b, int64_t e) {
-          for (int64_t r = b; r < e; ++r) dst[r] = src[r * stride];
-        });
+        plain.push_back({word, dst});
       }
     } else {  // String: source dictionary code -> first-appearance code of the result
       const Column& lex = set.tables.at(static_cast<std::size_t>(oc.lexicon_table))
@@ -731,6 +736,13 @@ ResultColumns materialise(const PipelineSet& set, const PipelineProgram& prog,
     }
     out.columns.push_back(std::move(col));
   }
+  if (!plain.empty())  // one pass over the row-major result for every plain column
+    parallel_rows(nrows, [&](int64_t b, int64_t e) {
+      for (int64_t r = b; r < e; ++r) {
+        const int64_t* row = rows + r * stride;
+        for (const Plain& pc : plain) pc.dst[r] = row[pc.word];
+      }
+    });
   return out;
 }
 
@@ -1157,6 +1169,7 @@ static QueryRun run_query(Engine& e, Engine::Impl& I, const PipelineSet& set,
         pm.launches += km.launches + 1;
         pm.grid = km.grid;
         pm.block = km.block;
+        if (out.flags & HAWK_FLAG_CHECK) throw Error("device bounds check failed in a build pipeline");
         if (out.flags & HAWK_FLAG_DUPLICATE)
           throw DuplicateKey("duplicate join build key in table '" + driver.name +
                              "' (join build sides must be key-unique)");
@@ -1240,6 +1253,7 @@ static QueryRun run_query(Engine& e, Engine::Impl& I, const PipelineSet& set,
       pm.launches += km.launches;
       pm.grid = km.grid;
       pm.block = km.block;
+      if (out.flags & HAWK_FLAG_CHECK) throw Error("device bounds check failed in the terminal pipeline");
       if (grouped && (out.flags & HAWK_FLAG_TABLE_FULL)) {
         // grow the table past the groups the device counted and rerun; the
         // group count is bounded by the input rows, so this terminates

@@ -41,3 +41,8 @@ for line in sass.splitlines():
 print(cub, sum(ops.values()), "instructions")
 for k, v in ops.most_common(40):
     print(f"{v:6d} {k}")
+print("memory / atomic opcodes:")
+for k, v in sorted(ops.items()):
+    if k.split(".")[0] in ("LDG", "STG", "LDS", "STS", "ATOM", "ATOMS", "ATOMG", "RED", "REDG", "REDS",
+                           "UBLKCP", "SYNCS", "LDGSTS", "UTMALDG"):
+        print(f"  {v:6d} {k}")

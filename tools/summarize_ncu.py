@@ -42,8 +42,10 @@ METRICS = {
 }
 summary = {}
 traffic_path = os.path.join(dst, "ncu_traffic.json")
-traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
-for rep in sorted(glob.glob(os.path.join(src, "full_*.ncu-rep"))):
+traffic = {k: v for k, v in (json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}).items()
+           if "@sf" in k}
+PATTERN = os.environ.get("NCU_PATTERN", "*@sf*")
+for rep in sorted(glob.glob(os.path.join(src, f"full_{PATTERN}.ncu-rep"))):
     q = os.path.basename(rep)[len("full_"):-len(".ncu-rep")]
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -65,7 +67,8 @@ for rep in sorted(glob.glob(os.path.join(src, "full_*.ncu-rep"))):
     except Exception:
         pass
 launches = {}
-for f in sorted(glob.glob(os.path.join(src, "launches_*.csv"))):
+SETUP = ("gen_column_kernel", "flush_read_kernel", "column_range_kernel")  # data generation / L2 hygiene / cached stats
+for f in sorted(glob.glob(os.path.join(src, f"launches_{PATTERN}.csv"))):
     q = os.path.basename(f)[len("launches_"):-len(".csv")]
     text = open(f).read()
     start = text.find('"ID"')
@@ -81,7 +84,9 @@ for f in sorted(glob.glob(os.path.join(src, "launches_*.csv"))):
         per[name][0] += 1
         per[name][1] += v * scale
     tot = sum(v[1] for v in per.values()) or 1.0
-    launches[q] = {k: {"launches": c, "us": round(t, 1), "share": round(t / tot, 3)}
+    query_tot = sum(v[1] for k, v in per.items() if not any(s in k for s in SETUP)) or 1.0
+    launches[q] = {k: {"launches": c, "us": round(t, 1), "share": round(t / tot, 3),
+                       "share_of_query_kernels": None if any(s in k for s in SETUP) else round(t / query_tot, 3)}
                    for k, (c, t) in sorted(per.items(), key=lambda kv: -kv[1][1])}
 os.makedirs(dst, exist_ok=True)
 json.dump(summary, open(os.path.join(dst, f"ncu_full_{tag}.json"), "w"), indent=1)
