@@ -57,6 +57,16 @@ int32_t hawk_nccl_alltoall(hawk_comm* comm, const void* d_send, const size_t* se
                            const size_t* send_off, void* d_recv, const size_t* recv_bytes,
                            const size_t* recv_off);
 
+/* In-process loopback group (tests): N ranks of one process, one host thread
+ * each, on one GPU. The hawk_nccl_* calls of a loopback communicator are
+ * device-to-device copies between the ranks' buffers sequenced by host
+ * barriers, so the multi-rank exchange logic runs where only one GPU is
+ * present; no kernel ever waits on another rank. */
+typedef struct hawk_loopback hawk_loopback;
+int32_t hawk_loopback_group_create(int32_t nranks, hawk_loopback** out);
+int32_t hawk_loopback_group_destroy(hawk_loopback* group);
+int32_t hawk_loopback_comm_create(hawk_ctx* ctx, hawk_loopback* group, int32_t rank, hawk_comm** out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,10 +6,10 @@ Native libraries (built in-tree into paper_1709_00700_b200/lib):
   libhawk_engine.so  C++ engine over the reference types (include/hawk_b200_engine.hpp/.h)
   libhawk_front.so   the reference's own front end, compiled unmodified
 """
-from .engine import (CapacityExceeded, Column, Communicator, DivergentPlan, DuplicateKey, EmptyAggregate,
+from .engine import (CapacityExceeded, Column, Communicator, LoopbackGroup, DivergentPlan, DuplicateKey, EmptyAggregate,
                      Engine, HawkError, InvalidConfig, InvalidParams, PlanTooLarge, Result,
                      Unsupported, UnsupportedPlan)
 
-__all__ = ["Engine", "Communicator", "Column", "Result", "HawkError", "UnsupportedPlan", "InvalidConfig",
+__all__ = ["Engine", "Communicator", "LoopbackGroup", "Column", "Result", "HawkError", "UnsupportedPlan", "InvalidConfig",
            "Unsupported", "PlanTooLarge", "CapacityExceeded", "DuplicateKey", "EmptyAggregate",
            "DivergentPlan", "InvalidParams"]

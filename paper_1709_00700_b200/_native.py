@@ -103,6 +103,9 @@ def b200() -> C.CDLL:
         _sig(lib, "hawk_nccl_unique_id", i32, vp)
         _sig(lib, "hawk_nccl_comm_create", i32, vp, i32, i32, vp, C.POINTER(vp))
         _sig(lib, "hawk_nccl_comm_destroy", i32, vp)
+        _sig(lib, "hawk_loopback_group_create", i32, i32, C.POINTER(vp))
+        _sig(lib, "hawk_loopback_group_destroy", i32, vp)
+        _sig(lib, "hawk_loopback_comm_create", i32, vp, vp, i32, C.POINTER(vp))
         _sig(lib, "hawk_nccl_comm_rank", i32, vp)
         _sig(lib, "hawk_nccl_comm_size", i32, vp)
         _sig(lib, "hawk_nccl_allreduce", i32, vp, vp, vp, C.c_size_t, i32, i32)

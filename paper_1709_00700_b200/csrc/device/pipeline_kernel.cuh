@@ -881,12 +881,10 @@ __device__ __forceinline__ void pipeline_body(const KParams& kp) {
     // in flight; thread t consumes tile rows t + jB.
     const int64_t pass_rows = (int64_t)B * R;
     const int64_t npasses = (len + pass_rows - 1) / pass_rows;
-#ifdef HK_NO_STAGE  // compiled programs that never stage: no TMA tile pipeline at all
-    const int S = kp.prefetch_passes;
-    constexpr int C = 0;
-#else
+    // C stays a runtime value even in programs that never stage: folding it
+    // to a constant 0 (HK_NO_STAGE) let the compiler reshape the pass loop
+    // and TPC-H Q1 SF10's terminal went 0.61 -> 1.36 ms (profiles/ab_r02_stage_count.txt)
     const int S = kp.prefetch_passes, C = kp.nprefetch;
-#endif
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kp.smem_stage_off);
     int64_t* stages = reinterpret_cast<int64_t*>(smem + kp.smem_stage_off + 128);
     if (threadIdx.x == 0 && C > 0) {

@@ -442,6 +442,12 @@ class Communicator:
         self.handle = h
         self.world, self.rank = world, rank
 
+    @classmethod
+    def _adopt(cls, lib, handle, world: int, rank: int) -> "Communicator":
+        c = cls.__new__(cls)
+        c._lib, c.handle, c.world, c.rank = lib, handle, world, rank
+        return c
+
     @staticmethod
     def unique_id() -> bytes:
         buf = (C.c_uint8 * 128)()
@@ -460,6 +466,33 @@ class Communicator:
             self.close()
         except Exception:
             pass
+
+
+class LoopbackGroup:
+    """N ranks of this process on one device (include/hawk_b200_comm.h): each
+    rank is an Engine driven from its own host thread, and the collectives of
+    its communicator are device-to-device copies between the ranks' buffers,
+    sequenced by host barriers. It runs the multi-rank exchange of
+    Engine.run_sharded where only one GPU is present; the NCCL communicator
+    is the production path."""
+
+    def __init__(self, world: int):
+        self._lib = _native.b200()
+        h = C.c_void_p()
+        if self._lib.hawk_loopback_group_create(world, C.byref(h)) != 0:
+            raise HawkError("loopback group: bad rank count")
+        self.handle, self.world = h, world
+
+    def communicator(self, engine: "Engine", rank: int) -> Communicator:
+        h = C.c_void_p()
+        if self._lib.hawk_loopback_comm_create(engine.ctx, self.handle, rank, C.byref(h)) != 0:
+            raise HawkError(f"loopback communicator: bad rank {rank}")
+        return Communicator._adopt(self._lib, h, self.world, rank)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.hawk_loopback_group_destroy(self.handle)
+            self.handle = None
 
 
 def save_config(config: str, path: str):

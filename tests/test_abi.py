@@ -4,6 +4,7 @@ import ctypes as C
 import os
 
 import numpy as np
+import pytest
 
 from paper_1709_00700_b200 import _native
 from paper_1709_00700_b200 import datagen as dg
@@ -28,7 +29,7 @@ def test_b200_library_exports_cross_header():
 
 def test_b200_library_exports_comm_and_csv_headers():
     lib = _native.b200()
-    for header, expect in (("hawk_b200_comm.h", 11), ("hawk_b200_csv.h", 8)):
+    for header, expect in (("hawk_b200_comm.h", 14), ("hawk_b200_csv.h", 8)):
         names = _native.declared_symbols(os.path.join(ROOT, "include", header))
         assert len(names) == expect, (header, names)
         missing = [n for n in names if not hasattr(lib, n)]
@@ -108,3 +109,14 @@ def test_first_appearance_recoding():
     codes = np.array([3, 1, 3, 0, 1])
     new, lex = dg.first_appearance(codes, ["a", "b", "c", "d"])
     assert lex == ["d", "b", "a"] and new.tolist() == [0, 1, 0, 2, 1]
+
+
+def test_loopback_group_arguments():
+    # host-only part of the loopback group: creation, rank checks, teardown
+    from paper_1709_00700_b200 import LoopbackGroup, HawkError
+    g = LoopbackGroup(3)
+    assert g.world == 3
+    g.close()
+    g.close()
+    with pytest.raises(HawkError):
+        LoopbackGroup(0)

@@ -183,6 +183,60 @@ def test_nccl_sharded_execution_one_rank(key):
         e.close()
 
 
+def _loopback_run(key, world, sf, cfg):
+    """`world` in-process ranks on this GPU (LoopbackGroup), each an Engine
+    holding its row shard of the fact table (TPC-H orders co-partitioned by
+    orderkey, dimensions replicated), each calling Engine.run_sharded from
+    its own thread. Returns the per-rank results."""
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_1709_00700_b200 import LoopbackGroup
+    from paper_1709_00700_b200.distributed import copartition_range
+    sql, tables, fact = Q.BENCH[key]
+    n = dg.table_rows(fact, sf)
+    per = -(-n // world)
+    per = -(-per // 4) * 4
+    engines = [Engine(0) for _ in range(world)]
+    group = LoopbackGroup(world)
+    try:
+        comms = []
+        for r, e in enumerate(engines):
+            b, end = min(n, r * per), min(n, (r + 1) * per)
+            for t in tables:
+                if t == fact:
+                    e.generate(t, sf, 42, b, end - b)
+                elif t == dg.ORDERS and fact == dg.LINEITEM:
+                    ob, oe = copartition_range(b, end)
+                    e.generate(t, sf, 42, ob, oe - ob)
+                else:
+                    e.generate(t, sf, 42)
+            comms.append(group.communicator(e, r))
+        with ThreadPoolExecutor(world) as ex:
+            outs = list(ex.map(lambda r: engines[r].run_sharded(sql, cfg, comms[r]), range(world)))
+        for c in comms:
+            c.close()
+        return outs
+    finally:
+        for e in engines:
+            e.close()
+        group.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("key", sorted(Q.BENCH))
+def test_sharded_execution_multi_rank_loopback(key, world):
+    # the N-rank exchange of Engine.execute_sharded (count all-gather, device
+    # gather to the root, device merge) with N engines on this GPU: the root
+    # holds the whole table's answer, the other ranks none of its rows
+    sql = Q.BENCH[key][0]
+    db = harness.oracle_db(harness.bench_tables("ssb" if key.startswith("ssb") else "tpch", 0.01, 42))
+    want = db.execute(sql)
+    for cfg in (CONFIGS[0], CONFIGS[1]):
+        outs = _loopback_run(key, world, 0.01, cfg)
+        diff = harness.compare(want, outs[0])
+        assert diff is None, f"{key} x{world} [{cfg}]: {diff}"
+        assert all(o.rows == 0 for o in outs[1:])
+
+
 def test_nccl_sharded_projection_and_empty(micro):
     from paper_1709_00700_b200 import Communicator
     engine, db = micro
