@@ -47,6 +47,7 @@ struct hawk_ctx {
   u64* d_ctrl = nullptr;
   u64* d_final = nullptr;  // HAWK_MAX_AGGS
   u64* h_readback = nullptr;  // pinned: ctrl words + AGGREGATE accumulators, one D2H
+  u64* h_upload = nullptr;    // pinned: their initial values, one H2D
   u64* d_partials = nullptr;
   size_t partials_cap = 0;
   int64_t* d_offsets = nullptr;
@@ -79,6 +80,18 @@ int ilog2_ceil(int64_t v) {
   int l = 0;
   while ((int64_t(1) << l) < v) ++l;
   return l;
+}
+
+// Waits for the stream by polling for up to 2 ms, then blocks: a pipeline's
+// read-back is usually microseconds away, and a blocking synchronise adds
+// its wake-up latency to every query.
+cudaError_t stream_wait(cudaStream_t s) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t e = cudaStreamQuery(s);
+    if (e != cudaErrorNotReady) return e;
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(2)) return cudaStreamSynchronize(s);
+  }
 }
 
 template <typename T>
@@ -499,10 +512,13 @@ int32_t hawk_b200_ctx_create(int32_t device, hawk_ctx** out) {
   int l2 = 0;
   HK_TRY(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device));
   ctx->l2_bytes = l2;
-  HK_TRY(cudaMalloc(&ctx->d_ctrl, 64));
-  HK_TRY(cudaMemset(ctx->d_ctrl, 0, 64));
-  HK_TRY(cudaMalloc(&ctx->d_final, HAWK_MAX_AGGS * 8));
+  // control words 0..7, then the AGGREGATE accumulators (d_final): one
+  // upload before and one read-back after a pipeline cover both
+  HK_TRY(cudaMalloc(&ctx->d_ctrl, (8 + HAWK_MAX_AGGS) * 8));
+  HK_TRY(cudaMemset(ctx->d_ctrl, 0, (8 + HAWK_MAX_AGGS) * 8));
+  ctx->d_final = ctx->d_ctrl + 8;
   HK_TRY(cudaMallocHost(&ctx->h_readback, (8 + HAWK_MAX_AGGS) * 8));
+  HK_TRY(cudaMallocHost(&ctx->h_upload, (8 + HAWK_MAX_AGGS) * 8));
   HK_TRY(cudaEventCreate(&ctx->ev0));
   HK_TRY(cudaEventCreate(&ctx->ev1));
   *out = ctx;
@@ -513,10 +529,11 @@ int32_t hawk_b200_ctx_destroy(hawk_ctx* ctx) {
   if (!ctx) return HAWK_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  for (void* p : {(void*)ctx->d_ctrl, (void*)ctx->d_final, (void*)ctx->d_partials,
+  for (void* p : {(void*)ctx->d_ctrl, (void*)ctx->d_partials,
                   (void*)ctx->d_offsets, (void*)ctx->d_out, (void*)ctx->d_groups, ctx->d_flush})
     if (p) cudaFree(p);
   if (ctx->h_readback) cudaFreeHost(ctx->h_readback);
+  if (ctx->h_upload) cudaFreeHost(ctx->h_upload);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
   cudaStreamDestroy(ctx->stream);
@@ -683,7 +700,7 @@ int32_t hawk_b200_memcpy_h2d(hawk_ctx* ctx, void* d_dst, const void* src, size_t
 }
 int32_t hawk_b200_memcpy_d2h(hawk_ctx* ctx, void* dst, const void* d_src, size_t bytes) {
   HK_TRY(cudaMemcpyAsync(dst, d_src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
-  HK_TRY(cudaStreamSynchronize(ctx->stream));
+  HK_TRY(stream_wait(ctx->stream));
   return HAWK_OK;
 }
 int32_t hawk_b200_memset(hawk_ctx* ctx, void* d_ptr, int32_t value, size_t bytes) {
@@ -893,6 +910,63 @@ int32_t hawk_b200_column_range(hawk_ctx* ctx, const int64_t* d_col, int64_t n, i
   return HAWK_OK;
 }
 
+int32_t hawk_b200_rows_pack_plan(hawk_ctx* ctx, const int64_t* d_rows, int64_t n, int32_t width,
+                                 hawk_packed* plan) {
+  if (!ctx || !plan || width < 1 || width > HAWK_MAX_WIDTH || n < 0 || (n > 0 && !d_rows))
+    return HAWK_ERR_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  std::memset(plan, 0, sizeof *plan);
+  plan->rows = n;
+  plan->width = width;
+  long long h[2 * HAWK_MAX_WIDTH];
+  for (int c = 0; c < width; ++c) {
+    h[2 * c] = 0x7fffffffffffffffll;
+    h[2 * c + 1] = (long long)0x8000000000000000ull;
+  }
+  if (n > 0) {
+    const int32_t st = ensure(ctx->d_partials, ctx->partials_cap, 16 * (size_t)width);
+    if (st != HAWK_OK) return st;
+    long long* d_out = reinterpret_cast<long long*>(ctx->d_partials);  // 2w words of scratch
+    HK_TRY(cudaMemcpyAsync(d_out, h, 16 * (size_t)width, cudaMemcpyHostToDevice, ctx->stream));
+    const int64_t blocks =
+        std::min<int64_t>((int64_t)ctx->sms * 4, std::max<int64_t>(1, (n * width + 255) / 256));
+    hk::rows_range_kernel<<<(unsigned)blocks, 256, 16 * (size_t)width, ctx->stream>>>(d_rows, n, width, d_out);
+    HK_TRY(cudaGetLastError());
+    HK_TRY(cudaMemcpyAsync(h, d_out, 16 * (size_t)width, cudaMemcpyDeviceToHost, ctx->stream));
+    HK_TRY(cudaStreamSynchronize(ctx->stream));
+  }
+  int64_t off = 0;
+  for (int c = 0; c < width; ++c) {
+    const uint64_t range = n > 0 ? (uint64_t)h[2 * c + 1] - (uint64_t)h[2 * c] : 0;
+    const int b = range == 0 ? 0 : range <= 0xffull ? 1 : range <= 0xffffull ? 2 : range <= 0xffffffffull ? 4 : 8;
+    plan->bytes[c] = b;
+    plan->base[c] = n > 0 ? (int64_t)h[2 * c] : 0;
+    plan->offset[c] = off;
+    off += ((int64_t)b * n + 15) & ~int64_t(15);
+  }
+  plan->total = off;
+  return HAWK_OK;
+}
+
+int32_t hawk_b200_rows_pack(hawk_ctx* ctx, const int64_t* d_rows, const hawk_packed* plan, void* d_out) {
+  if (!ctx || !plan || plan->width < 1 || plan->width > HAWK_MAX_WIDTH) return HAWK_ERR_ARGUMENT;
+  if (plan->rows == 0 || plan->total == 0) return HAWK_OK;
+  if (!d_rows || !d_out) return HAWK_ERR_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  hk::PackParams pp{};
+  pp.width = plan->width;
+  for (int c = 0; c < plan->width; ++c) {
+    pp.bytes[c] = plan->bytes[c];
+    pp.base[c] = plan->base[c];
+    pp.offset[c] = plan->offset[c];
+  }
+  const int64_t blocks = std::min<int64_t>((int64_t)ctx->sms * 8, (plan->rows + 255) / 256);
+  hk::rows_pack_kernel<<<(unsigned)blocks, 256, 0, ctx->stream>>>(d_rows, plan->rows, pp,
+                                                                   static_cast<unsigned char*>(d_out));
+  HK_TRY(cudaGetLastError());
+  return HAWK_OK;
+}
+
 int32_t hawk_b200_exclusive_prefix_sum(hawk_ctx* ctx, const int64_t* d_flags, int64_t n,
                                        int64_t* d_positions, int64_t* total) {
   int64_t* d_total = reinterpret_cast<int64_t*>(ctx->d_ctrl) + 3;
@@ -1064,7 +1138,10 @@ static int32_t run_pipeline_impl(hawk_ctx* ctx, const hawk_pipeline* pipe, const
   unsigned* d_counter = reinterpret_cast<unsigned*>(ctx->d_ctrl + 1);
   u64* d_cursor = ctx->d_ctrl + 2;
   int64_t* d_total = reinterpret_cast<int64_t*>(ctx->d_ctrl + 3);
-  HK_TRY(cudaMemsetAsync(ctx->d_ctrl, 0, 32, ctx->stream));  // flags, ticket, cursor, total
+  // flags, ticket, cursor, total (+ the AGGREGATE accumulators' identities
+  // below): uploaded from pinned memory right before the first launch
+  std::memset(ctx->h_upload, 0, 8 * 8);
+  size_t upload_words = 8;
 
   hk::KParams kp;
   std::memset(&kp, 0, sizeof kp);
@@ -1116,10 +1193,9 @@ static int32_t run_pipeline_impl(hawk_ctx* ctx, const hawk_pipeline* pipe, const
         st = ensure(ctx->d_partials, ctx->partials_cap, (size_t)shape.grid.x * std::max(p.naggs, 1) * 8);
         if (st != HAWK_OK) return st;
         kp.d_partials = ctx->d_partials;
-      } else {
-        u64 init[HAWK_MAX_AGGS];
-        for (int a = 0; a < p.naggs; ++a) init[a] = hk::agg_identity(p.aggs[a].fn, p.aggs[a].type);
-        HK_TRY(cudaMemcpyAsync(ctx->d_final, init, 8 * std::max(p.naggs, 1), cudaMemcpyHostToDevice, ctx->stream));
+      } else {  // d_final = d_ctrl + 8: the identities ride on the control-word upload
+        for (int a = 0; a < p.naggs; ++a) ctx->h_upload[8 + a] = hk::agg_identity(p.aggs[a].fn, p.aggs[a].type);
+        upload_words = 8 + (size_t)p.naggs;
       }
     }
     launches.push_back({role, shape});
@@ -1163,6 +1239,7 @@ static int32_t run_pipeline_impl(hawk_ctx* ctx, const hawk_pipeline* pipe, const
   }
 
   const double t_prepare = trace ? us_since(t_start) : 0.0;
+  HK_TRY(cudaMemcpyAsync(ctx->d_ctrl, ctx->h_upload, upload_words * 8, cudaMemcpyHostToDevice, ctx->stream));
   HK_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
   int nlaunch = 0;
   if (s == HAWK_MULTI_PASS) {
@@ -1229,11 +1306,9 @@ static int32_t run_pipeline_impl(hawk_ctx* ctx, const hawk_pipeline* pipe, const
   // one synchronising read-back: the control words and, for AGGREGATE, the
   // accumulators themselves (pinned)
   u64* ctrl = ctx->h_readback;
-  HK_TRY(cudaMemcpyAsync(ctrl, ctx->d_ctrl, 8 * 8, cudaMemcpyDeviceToHost, ctx->stream));
-  if (p.sink == HAWK_SINK_AGGREGATE && p.naggs > 0)
-    HK_TRY(cudaMemcpyAsync(ctrl + 8, ctx->d_final, (size_t)p.naggs * 8, cudaMemcpyDeviceToHost,
-                           ctx->stream));
-  HK_TRY(cudaStreamSynchronize(ctx->stream));
+  const size_t readback_words = 8 + (p.sink == HAWK_SINK_AGGREGATE ? (size_t)p.naggs : 0);
+  HK_TRY(cudaMemcpyAsync(ctrl, ctx->d_ctrl, readback_words * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  HK_TRY(stream_wait(ctx->stream));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
   if (trace)

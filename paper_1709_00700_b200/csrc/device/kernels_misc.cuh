@@ -90,6 +90,66 @@ __global__ void column_range_kernel(const int64_t* __restrict__ col, int64_t n, 
   }
 }
 
+// ---- narrowed result read-back (hawk_b200_rows_pack*) ---------------------------
+
+// per-column min / max of a row-major (n x w) block. Threads walk the flat
+// word index with a stride that is a multiple of w, so each thread stays on
+// one column; CTA partials meet in shared memory, one global atomic pair per
+// column per CTA. out[2c] = min, out[2c + 1] = max, preset by the host.
+__global__ void rows_range_kernel(const int64_t* __restrict__ rows, int64_t n, int w, long long* out) {
+  extern __shared__ long long sh[];  // 2w
+  for (int c = threadIdx.x; c < w; c += blockDim.x) {
+    sh[2 * c] = 0x7fffffffffffffffll;
+    sh[2 * c + 1] = (long long)0x8000000000000000ull;
+  }
+  __syncthreads();
+  const int64_t threads = (int64_t)gridDim.x * blockDim.x / w * w;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < threads) {
+    const int c = (int)(t % w);
+    long long lo = 0x7fffffffffffffffll, hi = (long long)0x8000000000000000ull;
+    for (int64_t i = t; i < n * w; i += threads) {
+      const long long v = (long long)__ldg(rows + i);
+      lo = min(lo, v);
+      hi = max(hi, v);
+    }
+    atomicMin(&sh[2 * c], lo);
+    atomicMax(&sh[2 * c + 1], hi);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < w; c += blockDim.x) {
+    atomicMin(out + 2 * c, sh[2 * c]);
+    atomicMax(out + 2 * c + 1, sh[2 * c + 1]);
+  }
+}
+
+struct PackParams {
+  int32_t width;
+  int32_t bytes[HAWK_MAX_WIDTH];
+  int64_t base[HAWK_MAX_WIDTH];
+  int64_t offset[HAWK_MAX_WIDTH];
+};
+
+// one thread per row: reads the row's words, writes each column's narrowed
+// value (coalesced across the warp per column)
+__global__ void rows_pack_kernel(const int64_t* __restrict__ rows, int64_t n, const __grid_constant__ PackParams pp,
+                                 unsigned char* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
+    const int64_t* row = rows + r * pp.width;
+    for (int c = 0; c < pp.width; ++c) {
+      const int b = pp.bytes[c];
+      if (b == 0) continue;
+      const u64 v = (u64)__ldg(row + c) - (u64)pp.base[c];
+      unsigned char* d = out + pp.offset[c];
+      if (b == 1) d[r] = (unsigned char)v;
+      else if (b == 2) reinterpret_cast<uint16_t*>(d)[r] = (uint16_t)v;
+      else if (b == 4) reinterpret_cast<uint32_t*>(d)[r] = (uint32_t)v;
+      else reinterpret_cast<u64*>(d)[r] = v;
+    }
+  }
+}
+
 // L2 flush by reading a buffer twice the L2 size: evicts the working set
 // while leaving only clean lines behind (a memset flush leaves dirty lines
 // whose write-back would land in the next timed kernel).

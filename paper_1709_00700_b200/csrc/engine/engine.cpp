@@ -161,6 +161,18 @@ struct Engine::Impl {
   // pinned host buffer for result read-back (D2H at full PCIe speed)
   int64_t* pinned = nullptr;
   size_t pinned_bytes = 0;
+  // narrowed read-back of a device row block into the pinned buffer
+  const int64_t* read_back_packed(const int64_t* d_rows, int64_t n, int width, hawk_packed* plan) {
+    check(hawk_b200_rows_pack_plan(ctx, d_rows, n, width, plan), "pack plan");
+    void* d_out = acquire(static_cast<size_t>(plan->total) + 16);
+    const int32_t st = hawk_b200_rows_pack(ctx, d_rows, plan, d_out);
+    int64_t* pin = host_buffer(static_cast<size_t>(plan->total) + 16);
+    const int32_t st2 = st != HAWK_OK ? st : hawk_b200_memcpy_d2h(ctx, pin, d_out, static_cast<size_t>(plan->total));
+    release(d_out);
+    check(st2, "packed D2H");
+    return pin;
+  }
+
   int64_t* host_buffer(size_t bytes) {
     if (bytes > pinned_bytes) {
       if (pinned) hawk_b200_host_free(pinned);
@@ -646,14 +658,17 @@ void parallel_rows(int64_t n, F&& f) {
 
 // HostFinalize: AVG division, output schema in SELECT order,
 // dictionary decoding (planner_reference.cpp:280-323), into plain columns.
+// `packed` (optional): `rows` is a narrowed block (hawk_b200_rows_pack) of
+// nrows x packed->width words, widened here on the way into the columns.
 ResultColumns materialise(const PipelineSet& set, const PipelineProgram& prog,
                           const LoweredProgram& lp, const int64_t* rows, int64_t nrows,
-                          int64_t stride, bool column_major) {
+                          int64_t stride, bool column_major, const hawk_packed* packed = nullptr) {
   const hawk_pipeline& p = lp.pipe;
   const int K = p.nkeys;
   const std::vector<OpAggregate>* aggs =
       prog.ops.back().kind == PipelineOpKind::Project ? nullptr : &prog.ops.back().aggregates;
   auto at = [&](int64_t r, int w) -> int64_t {
+    if (packed) return hawk_packed_at(packed, rows, r, w);
     return column_major ? rows[w * stride + r] : rows[r * stride + w];
   };
   if (p.sink == HAWK_SINK_AGGREGATE && nrows == 1) {
@@ -714,7 +729,24 @@ ResultColumns materialise(const PipelineSet& set, const PipelineProgram& prog,
         col.ints.resize(static_cast<std::size_t>(nrows));
         dst = col.ints.data();
       }
-      if (column_major) {
+      if (packed) {  // widen one narrowed column
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(rows) + packed->offset[word];
+        const int64_t base = packed->base[word];
+        const int bytes = packed->bytes[word];
+        parallel_rows(nrows, [&, src, base, bytes, dst](int64_t b, int64_t e) {
+          auto widen = [&](auto* s) {
+            for (int64_t r = b; r < e; ++r)
+              dst[r] = static_cast<int64_t>(static_cast<uint64_t>(base) + static_cast<uint64_t>(s[r]));
+          };
+          switch (bytes) {
+            case 0: std::fill(dst + b, dst + e, base); break;
+            case 1: widen(reinterpret_cast<const uint8_t*>(src)); break;
+            case 2: widen(reinterpret_cast<const uint16_t*>(src)); break;
+            case 4: widen(reinterpret_cast<const uint32_t*>(src)); break;
+            default: widen(reinterpret_cast<const uint64_t*>(src)); break;
+          }
+        });
+      } else if (column_major) {
         if (nrows > 0) std::memcpy(dst, rows + word * stride, static_cast<size_t>(nrows) * 8);
       } else {
         plain.push_back({word, dst});
@@ -745,6 +777,9 @@ ResultColumns materialise(const PipelineSet& set, const PipelineProgram& prog,
     });
   return out;
 }
+
+// results at least this large are read back narrowed (hawk_b200_rows_pack)
+constexpr size_t kPackBytes = size_t(1) << 20;
 
 uint64_t reseed(uint64_t seed, int attempt) {
   uint64_t x = seed + 0x9e3779b97f4a7c15ull * static_cast<uint64_t>(attempt + 1);
@@ -866,13 +901,17 @@ PartialResult Engine::execute_partial(const PipelineSet& set, const WorkloadConf
 
 // HAWK_TRACE=1: per-phase host time of run_query on stderr (the device is
 // synchronised at each mark, so queued kernels are charged to their phase)
+// HAWK_TRACE=1: per-phase times with a device synchronisation at each mark;
+// HAWK_TRACE=2: host time only (no synchronisation), the host-side overhead
 struct PhaseTrace {
-  bool on = std::getenv("HAWK_TRACE") != nullptr;
+  const char* env = std::getenv("HAWK_TRACE");
+  bool on = env != nullptr;
+  bool sync = env != nullptr && std::strcmp(env, "2") != 0;
   hawk_ctx* ctx = nullptr;
   std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
   void mark(const char* what) {
     if (!on) return;
-    hawk_b200_ctx_synchronize(ctx);
+    if (sync) hawk_b200_ctx_synchronize(ctx);
     const auto now = std::chrono::steady_clock::now();
     std::fprintf(stderr, "[hawk] %-28s %9.1f us\n", what,
                  std::chrono::duration<double, std::micro>(now - t).count());
@@ -1307,6 +1346,8 @@ static QueryRun run_query(Engine& e, Engine::Impl& I, const PipelineSet& set,
     const int64_t* pinned_rows = nullptr;
     int64_t nrows = 0, stride = 0;
     bool column_major = false;
+    hawk_packed packed{};
+    bool use_packed = false;
     if (lp.pipe.sink == HAWK_SINK_AGGREGATE) {
       host.resize(static_cast<std::size_t>(lp.pipe.naggs));
       if (out.h_values)  // read back with the control words
@@ -1321,7 +1362,11 @@ static QueryRun run_query(Engine& e, Engine::Impl& I, const PipelineSet& set,
       I.group_hint[hint_key] = out.rows;
       const size_t words = static_cast<size_t>(out.rows * out.width);
       const int64_t* rows_h = out.h_values;
-      if (words > 0 && !rows_h) {
+      if (words > 0 && !rows_h && !partial && words * 8 >= kPackBytes) {
+        // large results cross PCIe narrowed (hawk_b200_rows_pack)
+        rows_h = I.read_back_packed(out.d_values, out.rows, out.width, &packed);
+        use_packed = true;
+      } else if (words > 0 && !rows_h) {
         int64_t* pin = I.host_buffer(words * 8);
         check(hawk_b200_memcpy_d2h(ctx, pin, out.d_values, words * 8), "D2H");
         rows_h = pin;
@@ -1365,7 +1410,7 @@ static QueryRun run_query(Engine& e, Engine::Impl& I, const PipelineSet& set,
       }
     } else {
       result.columns = materialise(set, terminal, lp, pinned_rows ? pinned_rows : host.data(), nrows,
-                                   stride, column_major);
+                                   stride, column_major, use_packed ? &packed : nullptr);
       trace.mark("materialise");
     }
   } catch (...) {
@@ -1475,9 +1520,15 @@ ResultColumns Engine::execute_sharded(const PipelineSet& set_in, const WorkloadC
       hawk_output g{};
       check(hawk_b200_agg_table_extract(ctx_, &mq, &t, &g), "extract");
       const size_t words = static_cast<size_t>(g.rows * g.width);
-      int64_t* pin = words ? I.host_buffer(words * 8) : nullptr;
-      if (words) check(hawk_b200_memcpy_d2h(ctx_, pin, g.d_values, words * 8), "D2H");
-      out = materialise(set, q.terminal, q.lowered, pin, g.rows, g.width, false);
+      if (words * 8 >= kPackBytes) {  // narrowed read-back of a large merged result
+        hawk_packed plan{};
+        const int64_t* pin = I.read_back_packed(g.d_values, g.rows, g.width, &plan);
+        out = materialise(set, q.terminal, q.lowered, pin, g.rows, g.width, false, &plan);
+      } else {
+        int64_t* pin = words ? I.host_buffer(words * 8) : nullptr;
+        if (words) check(hawk_b200_memcpy_d2h(ctx_, pin, g.d_values, words * 8), "D2H");
+        out = materialise(set, q.terminal, q.lowered, pin, g.rows, g.width, false);
+      }
     } else {  // PROJECT: rank blocks of W columns each, concatenated column by column
       std::vector<int64_t> host(static_cast<std::size_t>(total) * W);
       int64_t at = 0;

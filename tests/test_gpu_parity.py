@@ -267,6 +267,64 @@ def test_column_range(engine):
             lib.hawk_b200_free(engine.ctx, ptr)
 
 
+def _unpack(plan, block, n, w):
+    out = np.zeros((n, w), np.int64)
+    for c in range(w):
+        b, off = plan.bytes[c], plan.offset[c]
+        dt = {1: np.uint8, 2: np.uint16, 4: np.uint32, 8: np.uint64}.get(b)
+        stored = np.zeros(n, np.uint64) if dt is None else \
+            np.frombuffer(block, dtype=dt, count=n, offset=off).astype(np.uint64)
+        with np.errstate(over="ignore"):
+            out[:, c] = (stored + np.uint64(plan.base[c] & (2**64 - 1))).view(np.int64)
+    return out
+
+
+@pytest.mark.parametrize("n,w", [(0, 3), (1, 1), (7, 20), (1000, 4), (300_001, 5)])
+def test_rows_pack_round_trip(engine, n, w):
+    # narrowed read-back (hawk_b200_rows_pack): constant columns take 0
+    # bytes, each other column the fewest of 1/2/4/8 bytes holding its range,
+    # including the full int64 range and float64 bit patterns
+    lib = _native.b200()
+    rng = np.random.default_rng(n + w)
+    rows = np.zeros((n, w), np.int64)
+    spans = [0, 1, 200, 60_000, 2**31, 2**40, None]
+    for c in range(w):
+        s = spans[c % len(spans)]
+        if s is None:
+            rows[:, c] = rng.integers(-2**63, 2**63 - 1, n, dtype=np.int64, endpoint=True)
+            if n >= 2:
+                rows[0, c], rows[1, c] = -2**63, 2**63 - 1
+        else:
+            rows[:, c] = -12345 + (rng.integers(0, s, n, dtype=np.int64) if s else 0)
+    if w >= 4 and n:
+        rows[:, 3] = rng.standard_normal(n).view(np.int64)
+    buf = C.c_void_p()
+    nbytes = max(8, rows.nbytes)
+    assert lib.hawk_b200_alloc(engine.ctx, nbytes, C.byref(buf)) == 0
+    out = C.c_void_p()
+    try:
+        if n:
+            assert lib.hawk_b200_memcpy_h2d(engine.ctx, buf, rows.ctypes.data, rows.nbytes) == 0
+        plan = _native.Packed()
+        assert lib.hawk_b200_rows_pack_plan(engine.ctx, buf, n, w, C.byref(plan)) == 0
+        assert plan.rows == n and plan.width == w
+        for c in range(w):
+            rng_c = int(rows[:, c].max()) - int(rows[:, c].min()) if n else 0
+            want = 0 if rng_c == 0 else 1 if rng_c < 2**8 else 2 if rng_c < 2**16 else 4 if rng_c < 2**32 else 8
+            assert plan.bytes[c] == want, (c, rng_c, plan.bytes[c])
+            assert plan.offset[c] % 16 == 0
+        assert lib.hawk_b200_alloc(engine.ctx, max(16, plan.total), C.byref(out)) == 0
+        assert lib.hawk_b200_rows_pack(engine.ctx, buf, C.byref(plan), out) == 0
+        block = np.zeros(max(16, plan.total), np.uint8)
+        if plan.total:
+            assert lib.hawk_b200_memcpy_d2h(engine.ctx, block.ctypes.data, out, plan.total) == 0
+        assert np.array_equal(_unpack(plan, block.tobytes(), n, w), rows)
+    finally:
+        lib.hawk_b200_free(engine.ctx, buf)
+        if out.value:
+            lib.hawk_b200_free(engine.ctx, out)
+
+
 @pytest.mark.parametrize("dense", [1, 0], ids=["dense-keys", "hash-only"])
 def test_group_by_dense_key_lookaside(bench_db, dense):
     # the dense key-index lookaside (small key domains) and the plain hash
