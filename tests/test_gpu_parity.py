@@ -726,3 +726,63 @@ def test_learner_within_125_of_full_exploration(micro, tmp_path):
         diff = harness.compare(db.execute(sql), engine.run(sql, cfg))
         assert diff is None, f"{sql} [{cfg}]: {diff}"
     engine.set_option("jit", 0)
+
+
+# ---- SPEC.md:334-335, :549 properties ------------------------------------------------
+
+def _with_dims(cfg: str, **kv) -> str:
+    """A config string with some dimensions of both halves replaced."""
+    def fix(half: str) -> str:
+        parts = half.split("/")
+        for k, v in kv.items():
+            if k == "pred":
+                parts = [v if p in ("branched", "predicated") else p for p in parts]
+            elif k == "u":
+                parts = [p for p in parts if not p.startswith("u=")] + ([f"u={v}"] if v > 1 else [])
+        return "/".join(parts)
+    return ";".join(fix(h) for h in cfg.split(";"))
+
+
+@pytest.mark.parametrize("n", [1, 7, 1001, 9999])
+def test_predicated_equals_branched_and_unrolled_equals_plain(n):
+    # random tables with n <= 10^4 rows (n mod u != 0 for u = 2, 4 except n=1):
+    # predicated == branched and u in {2, 4} == u = 1, under both program
+    # modes, every micro query, each result also equal to the oracle
+    e = Engine(0)
+    try:
+        tables = harness.micro_tables(n, 1000 + n)
+        harness.load_engine(e, tables)
+        db = harness.oracle_db(tables)
+        for jit in (1, 0):
+            e.set_option("jit", jit)
+            for base in CONFIGS[:4]:
+                for name, sql in harness.MICRO:
+                    want = db.execute(sql)
+                    sums = set()
+                    for cfg in (_with_dims(base, pred="branched", u=1), _with_dims(base, pred="predicated", u=1),
+                                _with_dims(base, pred="branched", u=2), _with_dims(base, pred="predicated", u=4)):
+                        got = e.run(sql, cfg)
+                        diff = harness.compare(want, got)
+                        assert diff is None, f"n={n} jit={jit} {name} [{cfg}]: {diff}"
+                        sums.add(harness.result_table(got).checksum())
+                    assert len(sums) == 1, f"n={n} jit={jit} {name} [{base}]: checksums differ {sums}"
+    finally:
+        e.close()
+
+
+def test_result_checksums_deterministic(bench_db):
+    # SPEC.md:549: result checksums are bit-identical across runs and across
+    # program modes (integer aggregates; AVG divides integer sums on the host)
+    import bench
+    which, engine, db = bench_db
+    for key, sql in harness.BENCH:
+        if key.startswith("ssb") != (which == "ssb"):
+            continue
+        sums = set()
+        for jit in (1, 0):
+            engine.set_option("jit", jit)
+            for cfg in (CONFIGS[0], CONFIGS[1], bench.default_config(key)):
+                for _ in range(2):
+                    sums.add(harness.result_table(engine.run(sql, cfg)).checksum())
+        assert sums == {db.execute(sql).checksum()}, f"{key}: {sums}"
+    engine.set_option("jit", 1)
