@@ -409,6 +409,18 @@ int32_t hawk_b200_run_pipeline_extract(hawk_ctx* ctx, const hawk_pipeline* pipel
                                        const hawk_variant* variant, int64_t* h_rows,
                                        int64_t h_cap_rows, hawk_output* out,
                                        hawk_metrics* metrics);
+/* Deferred build: a single-pass HASH_PUT pipeline launched like
+ * hawk_b200_run_pipeline, but without waiting for it. Its verdict (flags,
+ * inserted rows, the dense-index duplicate check, kernel time) is kept in
+ * `slot` (< HAWK_MAX_DEFERRED) on the device and read back by
+ * hawk_b200_deferred_collect after a later synchronising call, so a query's
+ * builds and its terminal pipeline reach the GPU back to back. Other sinks or
+ * strategies: HAWK_ERR_UNSUPPORTED. */
+#define HAWK_MAX_DEFERRED 16
+int32_t hawk_b200_run_pipeline_deferred(hawk_ctx* ctx, const hawk_pipeline* pipeline,
+                                        const hawk_variant* variant, int32_t slot);
+/* outputs (flags, rows) and metrics of slots 0..n-1 (synchronises) */
+int32_t hawk_b200_deferred_collect(hawk_ctx* ctx, int32_t n, hawk_output* outs, hawk_metrics* metrics);
 /* Layout-only twin of hawk_b200_agg_table_create (caller allocates). */
 int32_t hawk_b200_agg_table_layout(const hawk_pipeline* pipeline, int32_t impl, int32_t function,
                                    uint64_t seed, int64_t groups_bound, hawk_table* out,

@@ -59,6 +59,14 @@ struct hawk_ctx {
   void* d_flush = nullptr;
   size_t flush_bytes = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // deferred builds: per slot an event pair, a device verdict {flags, rows,
+  // index fill} and its pinned read-back
+  cudaEvent_t ev_def[HAWK_MAX_DEFERRED][2] = {};
+  u64* d_verdicts = nullptr;
+  u64* h_verdicts = nullptr;
+  int def_launches[HAWK_MAX_DEFERRED] = {};
+  int def_pending = 0;  // slots launched since the last collect
+  int def_ready = 0;    // slots whose verdicts rode on a pipeline's read-back
 };
 
 namespace {
@@ -534,6 +542,11 @@ int32_t hawk_b200_ctx_destroy(hawk_ctx* ctx) {
     if (p) cudaFree(p);
   if (ctx->h_readback) cudaFreeHost(ctx->h_readback);
   if (ctx->h_upload) cudaFreeHost(ctx->h_upload);
+  if (ctx->h_verdicts) cudaFreeHost(ctx->h_verdicts);
+  if (ctx->d_verdicts) cudaFree(ctx->d_verdicts);
+  for (auto& pr : ctx->ev_def)
+    for (cudaEvent_t e : pr)
+      if (e) cudaEventDestroy(e);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
   cudaStreamDestroy(ctx->stream);
@@ -1096,7 +1109,51 @@ int32_t hawk_b200_memcpy_d2d(hawk_ctx* ctx, void* d_dst, const void* d_src, size
 
 static int32_t run_pipeline_impl(hawk_ctx* ctx, const hawk_pipeline* pipe, const hawk_variant* v,
                                  hawk_output* out, hawk_metrics* metrics, int64_t* h_rows,
-                                 int64_t h_cap_rows);
+                                 int64_t h_cap_rows, int deferred_slot = -1);
+
+int32_t hawk_b200_run_pipeline_deferred(hawk_ctx* ctx, const hawk_pipeline* pipe, const hawk_variant* v,
+                                        int32_t slot) {
+  if (!ctx || !pipe || !v || slot < 0 || slot >= HAWK_MAX_DEFERRED) return HAWK_ERR_ARGUMENT;
+  if (pipe->sink != HAWK_SINK_HASH_PUT || v->strategy != HAWK_SINGLE_PASS) return HAWK_ERR_UNSUPPORTED;
+  cudaSetDevice(ctx->device);
+  if (!ctx->d_verdicts) {
+    HK_TRY(cudaMalloc(&ctx->d_verdicts, HAWK_MAX_DEFERRED * 4 * 8));
+    HK_TRY(cudaMallocHost(&ctx->h_verdicts, HAWK_MAX_DEFERRED * 4 * 8));
+  }
+  for (cudaEvent_t& e : ctx->ev_def[slot])
+    if (!e) HK_TRY(cudaEventCreate(&e));
+  hawk_output out{};
+  return run_pipeline_impl(ctx, pipe, v, &out, nullptr, nullptr, 0, slot);
+}
+
+int32_t hawk_b200_deferred_collect(hawk_ctx* ctx, int32_t n, hawk_output* outs, hawk_metrics* metrics) {
+  if (!ctx || n < 0 || n > HAWK_MAX_DEFERRED || (n > 0 && !outs)) return HAWK_ERR_ARGUMENT;
+  if (n == 0) return HAWK_OK;
+  if (!ctx->d_verdicts) return HAWK_ERR_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  if (ctx->def_ready < n) {
+    HK_TRY(cudaMemcpyAsync(ctx->h_verdicts, ctx->d_verdicts, (size_t)n * 4 * 8, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+    HK_TRY(stream_wait(ctx->stream));
+  }
+  ctx->def_pending = ctx->def_ready = 0;
+  for (int i = 0; i < n; ++i) {
+    const u64* w = ctx->h_verdicts + 4 * i;
+    std::memset(&outs[i], 0, sizeof outs[i]);
+    outs[i].flags = (int32_t)(w[0] & 0xffffffffu);
+    outs[i].rows = (int64_t)w[1];
+    if (w[3] && (int64_t)w[2] != outs[i].rows) outs[i].flags |= HAWK_FLAG_DUPLICATE;  // dense index fill
+    if (metrics) {
+      std::memset(&metrics[i], 0, sizeof metrics[i]);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ctx->ev_def[i][0], ctx->ev_def[i][1]);
+      metrics[i].kernel_ms = ms;
+      metrics[i].matches = outs[i].rows;
+      metrics[i].launches = ctx->def_launches[i];
+    }
+  }
+  return HAWK_OK;
+}
 
 int32_t hawk_b200_run_pipeline(hawk_ctx* ctx, const hawk_pipeline* pipe, const hawk_variant* v,
                                hawk_output* out, hawk_metrics* metrics) {
@@ -1112,7 +1169,7 @@ int32_t hawk_b200_run_pipeline_extract(hawk_ctx* ctx, const hawk_pipeline* pipe,
 
 static int32_t run_pipeline_impl(hawk_ctx* ctx, const hawk_pipeline* pipe, const hawk_variant* v,
                                  hawk_output* out, hawk_metrics* metrics, int64_t* h_rows,
-                                 int64_t h_cap_rows) {
+                                 int64_t h_cap_rows, int deferred_slot) {
   if (!ctx || !pipe || !v || !out) return HAWK_ERR_ARGUMENT;
   const hawk_pipeline& p = *pipe;
   if (p.nrows < 0 || p.ncolumns > HAWK_MAX_COLUMNS || p.nfilter > HAWK_MAX_FILTERS ||
@@ -1240,7 +1297,12 @@ static int32_t run_pipeline_impl(hawk_ctx* ctx, const hawk_pipeline* pipe, const
 
   const double t_prepare = trace ? us_since(t_start) : 0.0;
   HK_TRY(cudaMemcpyAsync(ctx->d_ctrl, ctx->h_upload, upload_words * 8, cudaMemcpyHostToDevice, ctx->stream));
-  HK_TRY(cudaEventRecord(ctx->ev0, ctx->stream));
+  const bool deferred = deferred_slot >= 0;
+  cudaEvent_t ev_begin = deferred ? ctx->ev_def[deferred_slot][0] : ctx->ev0;
+  cudaEvent_t ev_end = deferred ? ctx->ev_def[deferred_slot][1] : ctx->ev1;
+  HK_TRY(cudaEventRecord(ev_begin, ctx->stream));
+  const double t_upload = trace ? us_since(t_start) : 0.0;
+  double t_first_launch = 0.0;
   int nlaunch = 0;
   if (s == HAWK_MULTI_PASS) {
     // pass 1: per-CTA counts; pass 2: exclusive scan; pass 3: scatter
@@ -1255,6 +1317,7 @@ static int32_t run_pipeline_impl(hawk_ctx* ctx, const hawk_pipeline* pipe, const
     for (const Launch& l : launches) {
       st = launch(ctx, l.role, *v, kp, l.shape);
       if (st != HAWK_OK) return st;
+      if (trace && nlaunch == 0) t_first_launch = us_since(t_start);
       ++nlaunch;
     }
   }
@@ -1279,7 +1342,17 @@ static int32_t run_pipeline_impl(hawk_ctx* ctx, const hawk_pipeline* pipe, const
       HK_TRY(cudaGetLastError());
     }
   }
-  HK_TRY(cudaEventRecord(ctx->ev1, ctx->stream));
+  if (deferred) {  // the verdict stays on the device until hawk_b200_deferred_collect
+    hk::build_verdict_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_ctrl, p.sink_table.d_index != nullptr ? 1 : 0,
+                                                       ctx->d_verdicts + 4 * deferred_slot);
+    HK_TRY(cudaGetLastError());
+    HK_TRY(cudaEventRecord(ev_end, ctx->stream));
+    ctx->def_launches[deferred_slot] = nlaunch + 1;
+    ctx->def_pending = std::max(ctx->def_pending, deferred_slot + 1);
+    ctx->def_ready = 0;
+    return HAWK_OK;
+  }
+  HK_TRY(cudaEventRecord(ev_end, ctx->stream));
   // HASH_AGGREGATE with a host buffer: compact the groups right behind the
   // pipeline and read up to h_cap_rows of them back with the control words,
   // so small group-bys (TPC-H Q1: 4 groups) finish with one synchronisation
@@ -1303,17 +1376,25 @@ static int32_t run_pipeline_impl(hawk_ctx* ctx, const hawk_pipeline* pipe, const
                              ctx->stream));
   }
   const double t_launch = trace ? us_since(t_start) : 0.0;
+  const double t_first = t_first_launch;
   // one synchronising read-back: the control words and, for AGGREGATE, the
   // accumulators themselves (pinned)
   u64* ctrl = ctx->h_readback;
   const size_t readback_words = 8 + (p.sink == HAWK_SINK_AGGREGATE ? (size_t)p.naggs : 0);
   HK_TRY(cudaMemcpyAsync(ctrl, ctx->d_ctrl, readback_words * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (ctx->def_pending > 0) {  // verdicts of the deferred builds ride on the same synchronisation
+    HK_TRY(cudaMemcpyAsync(ctx->h_verdicts, ctx->d_verdicts, (size_t)ctx->def_pending * 4 * 8,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->def_ready = ctx->def_pending;
+  }
   HK_TRY(stream_wait(ctx->stream));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
   if (trace)
-    std::fprintf(stderr, "[hawk]   run_pipeline: prepare %.1f us, launched %.1f us, done %.1f us (kernels %.1f us)\n",
-                 t_prepare, t_launch, us_since(t_start), ms * 1e3);
+    std::fprintf(stderr,
+                 "[hawk]   run_pipeline: prepare %.1f us, uploaded %.1f us, first launch %.1f us, launched %.1f us, "
+                 "done %.1f us (kernels %.1f us)\n",
+                 t_prepare, t_upload, t_first, t_launch, us_since(t_start), ms * 1e3);
 
   std::memset(out, 0, sizeof *out);
   out->flags = (int32_t)(ctrl[0] & 0xffffffffu);

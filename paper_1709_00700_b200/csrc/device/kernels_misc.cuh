@@ -90,6 +90,15 @@ __global__ void column_range_kernel(const int64_t* __restrict__ col, int64_t n, 
   }
 }
 
+// a deferred build's verdict: flags, inserted rows, dense-index fill count
+// and whether there is an index (hawk_b200_deferred_collect)
+__global__ void build_verdict_kernel(const u64* __restrict__ ctrl, int has_index, u64* __restrict__ out) {
+  out[0] = ctrl[0] & 0xffffffffull;
+  out[1] = ctrl[2];
+  out[2] = ctrl[7];
+  out[3] = (u64)has_index;
+}
+
 // ---- narrowed result read-back (hawk_b200_rows_pack*) ---------------------------
 
 // per-column min / max of a row-major (n x w) block. Threads walk the flat

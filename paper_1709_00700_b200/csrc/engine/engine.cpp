@@ -119,6 +119,10 @@ struct Engine::Impl {
   // inside a cached PipelineSet): sizes the aggregation table and the
   // speculative read-back of the next run
   std::unordered_map<std::string, int64_t> group_hint;
+  // inserted / driver rows of each build program seen so far: orders the
+  // terminal's probes; a known build can be deferred (run_query_pass)
+  std::unordered_map<std::string, double> build_prob;
+  bool defer_builds = std::getenv("HAWK_SYNC_BUILDS") == nullptr;
   // key of a lowered program on its driver table: the op arrays' bytes (no
   // padding in these PODs), counts, and the driver's identity and size
   static std::string program_key(const hawk_pipeline& p, const DeviceTable& driver) {
@@ -1072,10 +1076,14 @@ static void materialise_cross(Engine::Impl& I, const PipelineSet& set,
   }
 }
 
+struct RetrySync {};  // thrown when a deferred build needs the synchronous path
+static QueryRun run_query_pass(Engine& e, Engine::Impl& I, const PipelineSet& set,
+                               const std::vector<VariantConfiguration>& configs, ExecutionMetrics* m,
+                               RunMode mode, bool defer);
+
 static QueryRun run_query(Engine& e, Engine::Impl& I, const PipelineSet& set,
                           const std::vector<VariantConfiguration>& configs, ExecutionMetrics* m,
                           RunMode mode) {
-  const bool partial = mode != RunMode::Full;
   if (set.terminal >= 0 && static_cast<std::size_t>(set.terminal) < set.pipelines.size() &&
       has_cross_join(set.pipelines[static_cast<std::size_t>(set.terminal)])) {
     require_device(e.ctx());
@@ -1100,6 +1108,21 @@ static QueryRun run_query(Engine& e, Engine::Impl& I, const PipelineSet& set,
       throw;
     }
   }
+  if (!I.defer_builds) return run_query_pass(e, I, set, configs, m, mode, false);
+  try {
+    return run_query_pass(e, I, set, configs, m, mode, true);
+  } catch (const RetrySync&) {  // a deferred cuckoo build failed: the synchronous path reseeds
+    return run_query_pass(e, I, set, configs, m, mode, false);
+  }
+}
+
+// One execution. defer: single-pass builds whose selectivity is known from an
+// earlier run are launched without waiting (hawk_b200_run_pipeline_deferred);
+// their verdicts are checked once the terminal pipeline has synchronised.
+static QueryRun run_query_pass(Engine& e, Engine::Impl& I, const PipelineSet& set,
+                               const std::vector<VariantConfiguration>& configs, ExecutionMetrics* m,
+                               RunMode mode, bool defer) {
+  const bool partial = mode != RunMode::Full;
   const auto t0 = std::chrono::steady_clock::now();
   PhaseTrace trace;
   trace.ctx = e.ctx();
@@ -1124,6 +1147,12 @@ static QueryRun run_query(Engine& e, Engine::Impl& I, const PipelineSet& set,
 
   std::map<int, hawk_table> built;  // descriptor -> join table
   std::map<int, double> match_prob; // descriptor -> inserted / build-table rows
+  struct Deferred {
+    std::size_t metrics_index;
+    std::string table, key;
+    int64_t rows;
+  };
+  std::vector<Deferred> deferred;   // builds launched without waiting, by slot
   std::vector<void*> scratch;       // blocks to return to the pool
   auto cleanup = [&]() {
     for (void* p : scratch) I.release(p);
@@ -1150,6 +1179,10 @@ static QueryRun run_query(Engine& e, Engine::Impl& I, const PipelineSet& set,
       PipelineMetrics pm;
       pm.variant = cfg.to_string();
       pm.rows_in = driver.rows;
+      const std::string build_key = Engine::Impl::program_key(lp.pipe, driver);
+      const auto known = I.build_prob.find(build_key);
+      const bool defer_this = defer && v.strategy == HAWK_SINGLE_PASS && known != I.build_prob.end() &&
+                              deferred.size() < HAWK_MAX_DEFERRED;
       // cuckoo builds that exceed 32 evictions rebuild with fresh seeds;
       // two failures raise CapacityExceeded
       // build keys over a dense range (every benchmark dimension key: SSB
@@ -1200,6 +1233,15 @@ static QueryRun run_query(Engine& e, Engine::Impl& I, const PipelineSet& set,
         }
         trace.mark("build: lower + table clear");
         lp.pipe.sink_table = t;
+        if (defer_this) {
+          check(hawk_b200_run_pipeline_deferred(ctx, &lp.pipe, &v, static_cast<int32_t>(deferred.size())),
+                "build pipeline");
+          deferred.push_back({M.pipelines.size(), driver.name, build_key, driver.rows});
+          built[put.descriptor] = t;
+          match_prob[put.descriptor] = known->second;
+          trace.mark("build: run_pipeline (deferred)");
+          break;
+        }
         hawk_output out{};
         hawk_metrics km{};
         check(hawk_b200_run_pipeline(ctx, &lp.pipe, &v, &out, &km), "build pipeline");
@@ -1223,6 +1265,7 @@ static QueryRun run_query(Engine& e, Engine::Impl& I, const PipelineSet& set,
         built[put.descriptor] = t;
         match_prob[put.descriptor] =
             out.rows >= 0 && driver.rows > 0 ? static_cast<double>(out.rows) / driver.rows : 1.0;
+        I.build_prob[build_key] = match_prob[put.descriptor];
         break;
       }
       M.pipelines.push_back(pm);
@@ -1308,6 +1351,26 @@ static QueryRun run_query(Engine& e, Engine::Impl& I, const PipelineSet& set,
         continue;
       }
       break;
+    }
+    if (!deferred.empty()) {  // the terminal's synchronisation covered the deferred builds
+      const std::size_t n = deferred.size();
+      std::vector<hawk_output> vo(n);
+      std::vector<hawk_metrics> vm(n);
+      check(hawk_b200_deferred_collect(ctx, static_cast<int32_t>(n), vo.data(), vm.data()), "deferred builds");
+      for (std::size_t i = 0; i < n; ++i) {
+        const Deferred& d = deferred[i];
+        if (vo[i].flags & HAWK_FLAG_CHECK) throw Error("device bounds check failed in a build pipeline");
+        if (vo[i].flags & HAWK_FLAG_DUPLICATE)
+          throw DuplicateKey("duplicate join build key in table '" + d.table +
+                             "' (join build sides must be key-unique)");
+        if (vo[i].flags & HAWK_FLAG_TABLE_FULL) throw CapacityExceeded("join table for '" + d.table + "' overflowed");
+        if (vo[i].flags & HAWK_FLAG_CUCKOO_FAIL) throw RetrySync{};
+        PipelineMetrics& bm = M.pipelines[d.metrics_index];
+        bm.kernel_ms += vm[i].kernel_ms;
+        bm.launches += vm[i].launches + 1;
+        bm.rows_out = vo[i].rows;
+        I.build_prob[d.key] = vo[i].rows >= 0 && d.rows > 0 ? static_cast<double>(vo[i].rows) / d.rows : 1.0;
+      }
     }
     result.terminal = terminal;
     result.lowered = lp;

@@ -21,7 +21,7 @@ from paper_1709_00700_b200 import queries as Q  # noqa: E402
 def main():
     import torch
     query, sf = sys.argv[1], float(sys.argv[2])
-    cfg = bench.default_config(query)
+    cfg = os.environ.get("AB_CONFIG") or bench.default_config(query)
     e = Engine(0)
     e.set_option("jit", 1)
     bench.load_tables(e, query, sf, 42, 0, 1)
