@@ -183,42 +183,91 @@ def test_nccl_sharded_execution_one_rank(key):
         e.close()
 
 
-def _loopback_run(key, world, sf, cfg):
-    """`world` in-process ranks on this GPU (LoopbackGroup), each an Engine
-    holding its row shard of the fact table (TPC-H orders co-partitioned by
-    orderkey, dimensions replicated), each calling Engine.run_sharded from
-    its own thread. Returns the per-rank results."""
-    from concurrent.futures import ThreadPoolExecutor
+def _loopback_engines(world, load):
+    """`world` in-process ranks on this GPU (LoopbackGroup): one Engine per
+    rank, loaded by load(engine, rank). Returns (engines, communicators, group)."""
     from paper_1709_00700_b200 import LoopbackGroup
+    engines = [Engine(0) for _ in range(world)]
+    group = LoopbackGroup(world)
+    comms = []
+    for r, e in enumerate(engines):
+        load(e, r)
+        comms.append(group.communicator(e, r))
+    return engines, comms, group
+
+
+def _loopback_query(engines, comms, sql, cfg):
+    """Engine.run_sharded on every rank, each from its own thread."""
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(len(engines)) as ex:
+        return list(ex.map(lambda r: engines[r].run_sharded(sql, cfg, comms[r]), range(len(engines))))
+
+
+def _loopback_close(engines, comms, group):
+    for c in comms:
+        c.close()
+    for e in engines:
+        e.close()
+    group.close()
+
+
+def _loopback_run(key, world, sf, cfg):
+    """Each rank holds its row shard of the fact table (TPC-H orders
+    co-partitioned by orderkey, dimensions replicated). Returns the per-rank
+    results."""
     from paper_1709_00700_b200.distributed import copartition_range
     sql, tables, fact = Q.BENCH[key]
     n = dg.table_rows(fact, sf)
     per = -(-n // world)
     per = -(-per // 4) * 4
-    engines = [Engine(0) for _ in range(world)]
-    group = LoopbackGroup(world)
+
+    def load(e, r):
+        b, end = min(n, r * per), min(n, (r + 1) * per)
+        for t in tables:
+            if t == fact:
+                e.generate(t, sf, 42, b, end - b)
+            elif t == dg.ORDERS and fact == dg.LINEITEM:
+                ob, oe = copartition_range(b, end)
+                e.generate(t, sf, 42, ob, oe - ob)
+            else:
+                e.generate(t, sf, 42)
+    state = _loopback_engines(world, load)
     try:
-        comms = []
-        for r, e in enumerate(engines):
-            b, end = min(n, r * per), min(n, (r + 1) * per)
-            for t in tables:
-                if t == fact:
-                    e.generate(t, sf, 42, b, end - b)
-                elif t == dg.ORDERS and fact == dg.LINEITEM:
-                    ob, oe = copartition_range(b, end)
-                    e.generate(t, sf, 42, ob, oe - ob)
-                else:
-                    e.generate(t, sf, 42)
-            comms.append(group.communicator(e, r))
-        with ThreadPoolExecutor(world) as ex:
-            outs = list(ex.map(lambda r: engines[r].run_sharded(sql, cfg, comms[r]), range(world)))
-        for c in comms:
-            c.close()
-        return outs
+        return _loopback_query(state[0], state[1], sql, cfg)
     finally:
-        for e in engines:
-            e.close()
-        group.close()
+        _loopback_close(*state)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_micro_queries_multi_rank_loopback(world):
+    # every sink kind through the N-rank exchange: projections (Listings 1/2:
+    # blocks concatenated), the many-group global hash (Listing 9: rows merged
+    # through the device aggregation table), joins and non-grouped aggregates;
+    # lineorder row-sharded with global row offsets, dimensions replicated
+    tables = harness.micro_tables(100_000, 7)
+    db = harness.oracle_db(tables)
+    lo = tables[0]
+    cols = lo.columns()
+    n = lo.rows
+    per = -(-n // world)
+
+    def load(e, r):
+        b, end = min(n, r * per), min(n, (r + 1) * per)
+        shard = [Column(c.name, c.kind, np.asarray(c.values)[b:end], getattr(c, "lexicon", None)) for c in cols]
+        e.put_table(lo.name, shard, row_offset=b)
+        for t in tables[1:]:
+            e.put_table(t.name, t.columns(), distinct=t.distinct())
+    engines, comms, group = _loopback_engines(world, load)
+    try:
+        for name, sql in harness.MICRO:
+            want = db.execute(sql)
+            for cfg in (CONFIGS[0], CONFIGS[1], CONFIGS[3]):
+                outs = _loopback_query(engines, comms, sql, cfg)
+                diff = harness.compare(want, outs[0])
+                assert diff is None, f"{name} x{world} [{cfg}]: {diff}"
+                assert all(o.rows == 0 for o in outs[1:]), name
+    finally:
+        _loopback_close(engines, comms, group)
 
 
 @pytest.mark.parametrize("world", [2, 3])
