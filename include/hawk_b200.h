@@ -373,6 +373,13 @@ int32_t hawk_b200_rows_pack_plan(hawk_ctx* ctx, const int64_t* d_rows, int64_t n
                                  hawk_packed* plan);
 /* writes plan->total bytes at d_out (async on the context stream) */
 int32_t hawk_b200_rows_pack(hawk_ctx* ctx, const int64_t* d_rows, const hawk_packed* plan, void* d_out);
+/* Starts the read-back of a packed block column by column: one async D2H per
+ * column into h_block (pinned, plan->total bytes), issued in `order`
+ * (n column indices); hawk_b200_rows_pack_wait(w) returns once column w is
+ * on the host, so the host widens one column while the next is in flight. */
+int32_t hawk_b200_rows_pack_fetch(hawk_ctx* ctx, const hawk_packed* plan, const void* d_block, void* h_block,
+                                  const int32_t* order, int32_t n);
+int32_t hawk_b200_rows_pack_wait(hawk_ctx* ctx, int32_t w);
 /* host side: word `w` of row `r` of a packed block */
 static inline int64_t hawk_packed_at(const hawk_packed* plan, const void* block, int64_t r, int32_t w) {
   const unsigned char* c = (const unsigned char*)block + plan->offset[w];

@@ -66,6 +66,7 @@ struct hawk_ctx {
   u64* h_verdicts = nullptr;
   int def_launches[HAWK_MAX_DEFERRED] = {};
   int def_pending = 0;  // slots launched since the last collect
+  cudaEvent_t ev_col[HAWK_MAX_WIDTH] = {};  // per-column read-back completion (rows_pack_fetch)
   int def_ready = 0;    // slots whose verdicts rode on a pipeline's read-back
 };
 
@@ -547,6 +548,8 @@ int32_t hawk_b200_ctx_destroy(hawk_ctx* ctx) {
   for (auto& pr : ctx->ev_def)
     for (cudaEvent_t e : pr)
       if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->ev_col)
+    if (e) cudaEventDestroy(e);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
   cudaStreamDestroy(ctx->stream);
@@ -978,6 +981,34 @@ int32_t hawk_b200_rows_pack(hawk_ctx* ctx, const int64_t* d_rows, const hawk_pac
                                                                    static_cast<unsigned char*>(d_out));
   HK_TRY(cudaGetLastError());
   return HAWK_OK;
+}
+
+int32_t hawk_b200_rows_pack_fetch(hawk_ctx* ctx, const hawk_packed* plan, const void* d_block, void* h_block,
+                                  const int32_t* order, int32_t n) {
+  if (!ctx || !plan || !order || n < 0 || n > plan->width || (plan->total > 0 && (!d_block || !h_block)))
+    return HAWK_ERR_ARGUMENT;
+  cudaSetDevice(ctx->device);
+  for (int i = 0; i < n; ++i) {
+    const int w = order[i];
+    if (w < 0 || w >= plan->width) return HAWK_ERR_ARGUMENT;
+    if (!ctx->ev_col[w]) HK_TRY(cudaEventCreateWithFlags(&ctx->ev_col[w], cudaEventDisableTiming));
+    const size_t bytes = (size_t)plan->bytes[w] * (size_t)plan->rows;
+    if (bytes)
+      HK_TRY(cudaMemcpyAsync(static_cast<char*>(h_block) + plan->offset[w],
+                             static_cast<const char*>(d_block) + plan->offset[w], bytes, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    HK_TRY(cudaEventRecord(ctx->ev_col[w], ctx->stream));
+  }
+  return HAWK_OK;
+}
+
+int32_t hawk_b200_rows_pack_wait(hawk_ctx* ctx, int32_t w) {
+  if (!ctx || w < 0 || w >= HAWK_MAX_WIDTH || !ctx->ev_col[w]) return HAWK_ERR_ARGUMENT;
+  for (;;) {  // poll: the columns arrive within a millisecond or two
+    const cudaError_t e = cudaEventQuery(ctx->ev_col[w]);
+    if (e == cudaSuccess) return HAWK_OK;
+    if (e != cudaErrorNotReady) return cuda_status(e);
+  }
 }
 
 int32_t hawk_b200_exclusive_prefix_sum(hawk_ctx* ctx, const int64_t* d_flags, int64_t n,

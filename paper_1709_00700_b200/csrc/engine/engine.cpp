@@ -165,15 +165,20 @@ struct Engine::Impl {
   // pinned host buffer for result read-back (D2H at full PCIe speed)
   int64_t* pinned = nullptr;
   size_t pinned_bytes = 0;
-  // narrowed read-back of a device row block into the pinned buffer
-  const int64_t* read_back_packed(const int64_t* d_rows, int64_t n, int width, hawk_packed* plan) {
+  // narrowed read-back of a device row block into the pinned buffer: packs
+  // it, then starts one async copy per column in `order` (the columns the
+  // result reads, in the order materialise reads them); materialise waits
+  // for each column (hawk_b200_rows_pack_wait) as it gets to it
+  const int64_t* read_back_packed(const int64_t* d_rows, int64_t n, int width, hawk_packed* plan,
+                                  const std::vector<int32_t>& order) {
     check(hawk_b200_rows_pack_plan(ctx, d_rows, n, width, plan), "pack plan");
     void* d_out = acquire(static_cast<size_t>(plan->total) + 16);
-    const int32_t st = hawk_b200_rows_pack(ctx, d_rows, plan, d_out);
+    int32_t st = hawk_b200_rows_pack(ctx, d_rows, plan, d_out);
     int64_t* pin = host_buffer(static_cast<size_t>(plan->total) + 16);
-    const int32_t st2 = st != HAWK_OK ? st : hawk_b200_memcpy_d2h(ctx, pin, d_out, static_cast<size_t>(plan->total));
-    release(d_out);
-    check(st2, "packed D2H");
+    if (st == HAWK_OK)
+      st = hawk_b200_rows_pack_fetch(ctx, plan, d_out, pin, order.data(), static_cast<int32_t>(order.size()));
+    release(d_out);  // later users of the block are ordered after the copies on the stream
+    check(st, "packed D2H");
     return pin;
   }
 
@@ -662,13 +667,42 @@ void parallel_rows(int64_t n, F&& f) {
 
 // HostFinalize: AVG division, output schema in SELECT order,
 // dictionary decoding (planner_reference.cpp:280-323), into plain columns.
+// The row words the result's output columns read, in the order materialise
+// reads them (AVG: the SUM, then the COUNT).
+std::vector<int32_t> consumed_words(const PipelineProgram& prog, const LoweredProgram& lp) {
+  const hawk_pipeline& p = lp.pipe;
+  const int off = p.sink == HAWK_SINK_HASH_AGGREGATE ? p.nkeys : 0;
+  std::vector<int32_t> out;
+  auto add = [&](int w) {
+    if (std::find(out.begin(), out.end(), w) == out.end()) out.push_back(w);
+  };
+  for (const OutputColumn& oc : prog.output) {
+    switch (oc.source) {
+      case OutputColumn::Source::ProjectAttr:
+      case OutputColumn::Source::GroupKey: add(oc.index); break;
+      case OutputColumn::Source::Aggregate: add(off + lp.agg_slot.at(static_cast<std::size_t>(oc.index))); break;
+      case OutputColumn::Source::AvgDivide:
+        add(off + lp.agg_slot.at(static_cast<std::size_t>(oc.index)));
+        add(off + lp.agg_slot.at(static_cast<std::size_t>(oc.index2)));
+        break;
+    }
+  }
+  return out;
+}
+
 // `packed` (optional): `rows` is a narrowed block (hawk_b200_rows_pack) of
-// nrows x packed->width words, widened here on the way into the columns.
+// nrows x packed->width words, widened here on the way into the columns;
+// with `fetch_ctx` its columns are still arriving (hawk_b200_rows_pack_fetch)
+// and each is waited for when it is first read.
 ResultColumns materialise(const PipelineSet& set, const PipelineProgram& prog,
                           const LoweredProgram& lp, const int64_t* rows, int64_t nrows,
-                          int64_t stride, bool column_major, const hawk_packed* packed = nullptr) {
+                          int64_t stride, bool column_major, const hawk_packed* packed = nullptr,
+                          hawk_ctx* fetch_ctx = nullptr) {
   const hawk_pipeline& p = lp.pipe;
   const int K = p.nkeys;
+  auto arrive = [&](int w) {
+    if (packed && fetch_ctx) check(hawk_b200_rows_pack_wait(fetch_ctx, w), "packed D2H");
+  };
   const std::vector<OpAggregate>* aggs =
       prog.ops.back().kind == PipelineOpKind::Project ? nullptr : &prog.ops.back().aggregates;
   auto at = [&](int64_t r, int w) -> int64_t {
@@ -714,6 +748,8 @@ ResultColumns materialise(const PipelineSet& set, const PipelineProgram& prog,
       const int sl = lp.agg_slot.at(static_cast<std::size_t>(oc.index));
       const int c = lp.agg_slot.at(static_cast<std::size_t>(oc.index2));
       const int off = p.sink == HAWK_SINK_HASH_AGGREGATE ? K : 0;
+      arrive(off + sl);
+      arrive(off + c);
       col.kind = ColumnKind::Float64;
       col.floats.resize(static_cast<std::size_t>(nrows));
       parallel_rows(nrows, [&](int64_t b, int64_t e) {
@@ -734,6 +770,7 @@ ResultColumns materialise(const PipelineSet& set, const PipelineProgram& prog,
         dst = col.ints.data();
       }
       if (packed) {  // widen one narrowed column
+        arrive(word);
         const unsigned char* src = reinterpret_cast<const unsigned char*>(rows) + packed->offset[word];
         const int64_t base = packed->base[word];
         const int bytes = packed->bytes[word];
@@ -760,6 +797,7 @@ ResultColumns materialise(const PipelineSet& set, const PipelineProgram& prog,
                               ->column(static_cast<std::size_t>(oc.lexicon_column));
       std::unordered_map<int64_t, int64_t> recode;
       col.ints.resize(static_cast<std::size_t>(nrows));
+      arrive(word);
       for (int64_t r = 0; r < nrows; ++r) {
         const int64_t raw = at(r, word);
         auto it = recode.find(raw);
@@ -1427,7 +1465,7 @@ static QueryRun run_query_pass(Engine& e, Engine::Impl& I, const PipelineSet& se
       const int64_t* rows_h = out.h_values;
       if (words > 0 && !rows_h && !partial && words * 8 >= kPackBytes) {
         // large results cross PCIe narrowed (hawk_b200_rows_pack)
-        rows_h = I.read_back_packed(out.d_values, out.rows, out.width, &packed);
+        rows_h = I.read_back_packed(out.d_values, out.rows, out.width, &packed, consumed_words(terminal, lp));
         use_packed = true;
       } else if (words > 0 && !rows_h) {
         int64_t* pin = I.host_buffer(words * 8);
@@ -1473,7 +1511,8 @@ static QueryRun run_query_pass(Engine& e, Engine::Impl& I, const PipelineSet& se
       }
     } else {
       result.columns = materialise(set, terminal, lp, pinned_rows ? pinned_rows : host.data(), nrows,
-                                   stride, column_major, use_packed ? &packed : nullptr);
+                                   stride, column_major, use_packed ? &packed : nullptr,
+                                   use_packed ? ctx : nullptr);
       trace.mark("materialise");
     }
   } catch (...) {
@@ -1585,8 +1624,9 @@ ResultColumns Engine::execute_sharded(const PipelineSet& set_in, const WorkloadC
       const size_t words = static_cast<size_t>(g.rows * g.width);
       if (words * 8 >= kPackBytes) {  // narrowed read-back of a large merged result
         hawk_packed plan{};
-        const int64_t* pin = I.read_back_packed(g.d_values, g.rows, g.width, &plan);
-        out = materialise(set, q.terminal, q.lowered, pin, g.rows, g.width, false, &plan);
+        const int64_t* pin =
+            I.read_back_packed(g.d_values, g.rows, g.width, &plan, consumed_words(q.terminal, q.lowered));
+        out = materialise(set, q.terminal, q.lowered, pin, g.rows, g.width, false, &plan, ctx_);
       } else {
         int64_t* pin = words ? I.host_buffer(words * 8) : nullptr;
         if (words) check(hawk_b200_memcpy_d2h(ctx_, pin, g.d_values, words * 8), "D2H");
