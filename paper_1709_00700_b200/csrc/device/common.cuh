@@ -67,13 +67,31 @@ __device__ __forceinline__ u64 ldg64(const void* p) {
 // dimension structures (key bitmaps, join tables) the probes hit.
 // (asm volatile: these sit under validity predicates and must not be hoisted
 // speculatively past them)
+// They also carry an L2 evict_first cache hint: a fact column is read once,
+// and without the hint the scan evicts the dimension indexes and bitmaps the
+// probes need from L2 (HK_STREAM_L2_NORMAL: plain L2 policy, for A/B).
+__device__ __forceinline__ u64 l2_evict_first() {
+  u64 pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ u64 ldg64_stream(const void* p) {
   u64 v;
+#ifdef HK_STREAM_L2_NORMAL
   asm volatile("ld.global.nc.L1::no_allocate.b64 %0, [%1];" : "=l"(v) : "l"(p));
+#else
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b64 %0, [%1], %2;"
+               : "=l"(v) : "l"(p), "l"(l2_evict_first()));
+#endif
   return v;
 }
 __device__ __forceinline__ void ldg128_stream(const void* p, u64& a, u64& b) {
+#ifdef HK_STREAM_L2_NORMAL
   asm volatile("ld.global.nc.L1::no_allocate.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+#else
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.b64 {%0, %1}, [%2], %3;"
+               : "=l"(a), "=l"(b) : "l"(p), "l"(l2_evict_first()));
+#endif
 }
 // probe-side reads of small, hot structures: keep in L1
 __device__ __forceinline__ u64 ldg64_keep(const void* p) {
