@@ -835,3 +835,38 @@ def test_result_checksums_deterministic(bench_db):
                     sums.add(harness.result_table(engine.run(sql, cfg)).checksum())
         assert sums == {db.execute(sql).checksum()}, f"{key}: {sums}"
     engine.set_option("jit", 1)
+
+
+# ---- seeded random queries (tests/fuzz_sql.py) ------------------------------------------
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_random_queries_match_oracle(micro, seed):
+    # 40 random queries per seed (HAWK_FUZZ_QUERIES overrides; 4 x 75 passed
+    # in round 2) in the reference grammar (filters, string
+    # equality, arithmetic incl. division and float literals, all aggregate
+    # functions, one/two-key group-bys incl. many groups, projections, 0-2
+    # joins); each on two random variants compiled and every fourth also
+    # interpreted; the oracle's EmptyAggregate must be raised as well
+    import random
+    import fuzz_sql
+    engine, db = micro
+    rng = random.Random(seed)
+    try:
+        for i in range(int(os.environ.get("HAWK_FUZZ_QUERIES", "40"))):
+            sql = fuzz_sql.random_query(rng)
+            cfgs = rng.sample(CONFIGS, 2)
+            try:
+                want = db.execute(sql)
+            except OraError as e:
+                assert e.cls == 7, f"unexpected oracle error {e.cls} for {sql}: {e}"
+                engine.set_option("jit", 1)
+                with pytest.raises(EmptyAggregate):
+                    engine.run(sql, cfgs[0])
+                continue
+            for jit in ((1, 0) if i % 4 == 0 else (1,)):
+                engine.set_option("jit", jit)
+                for cfg in cfgs:
+                    diff = harness.compare(want, engine.run(sql, cfg))
+                    assert diff is None, f"seed {seed} #{i} jit={jit} {sql} [{cfg}]: {diff}"
+    finally:
+        engine.set_option("jit", 0)
