@@ -37,6 +37,7 @@ struct hawk_ctx {
   int drain_rows = 0;       // compiled, compacted: queued rows per lane per drain (0 = auto)
   int split_bits = 1;       // compiled, compacted: key bitmaps for the first (1) / every (2) probe
   int checked = 0;          // compiled programs with device bounds checks
+  int index_atomic = 1;     // compiled single-pass builds: atomic dense-index inserts (no count pass)
   // COALESCED: stage pass tiles in smem with TMA. Off by default since the
   // private-accumulator group-by: TPC-H Q1 SF10 terminal 0.744 -> 0.712 ms
   // unstaged without the pass barrier, TPC-H Q6 unchanged (0.0343 ms both;
@@ -389,6 +390,12 @@ int32_t prepare(hawk_ctx* ctx, const hawk_pipeline& pipe, const hawk_variant& v,
   kp.split_drain = !kp.split ? 1 : ctx->drain_rows > 0 ? ctx->drain_rows : auto_drain(pipe);
   kp.split_bits = kp.split ? ctx->split_bits : 0;
   kp.checked = ctx->checked;
+  // small dense indexes: the count pass is mostly launch and tail; large ones
+  // (TPC-H Q3's orders, 150M entries) are faster with plain stores + the pass:
+  // Q3 SF100 orders build 0.93 ms plain vs 2.46 ms atomic, SSB Q1.1 date
+  // build 0.022 vs 0.015 ms (profiles/ab_r02_index_atomic.txt)
+  kp.index_atomic = ctx->jit && ctx->index_atomic && role == hk::K_PUT_SINGLE &&
+                    pipe.sink_table.d_index != nullptr && pipe.sink_table.index_span <= (int64_t(1) << 21);
   // thread-private group-by accumulators (scan + group-by, TPC-H Q1) take
   // more registers than 3 CTAs/SM leave; 2 CTAs of 256 threads measured
   // 0.67 vs 0.79 ms on Q1 SF10 (profiles/ab_r02_q1_min_ctas.txt)
@@ -666,6 +673,10 @@ int32_t hawk_b200_ctx_set_option(hawk_ctx* ctx, const char* name, int64_t value)
     ctx->checked = value != 0;
     return HAWK_OK;
   }
+  if (std::strcmp(name, "index_atomic") == 0) {
+    ctx->index_atomic = value != 0;
+    return HAWK_OK;
+  }
   if (std::strcmp(name, "split_bits") == 0) {
     ctx->split_bits = (int)std::max<int64_t>(0, std::min<int64_t>(value, 2));
     return HAWK_OK;
@@ -685,7 +696,7 @@ int32_t hawk_b200_ctx_get_option(hawk_ctx* ctx, const char* name, int64_t* value
       {"stage_probes", ctx->stage_probes}, {"pass_sync", ctx->pass_sync}, {"jit", ctx->jit},
       {"stage", ctx->stage}, {"priv_groups", ctx->priv_groups}, {"dense_join", ctx->dense_join},
       {"drain_rows", ctx->drain_rows}, {"split_bits", ctx->split_bits},
-      {"checked", ctx->checked}};
+      {"checked", ctx->checked}, {"index_atomic", ctx->index_atomic}};
   for (const auto& o : opts)
     if (std::strcmp(name, o.n) == 0) {
       *value = o.v;
@@ -1366,7 +1377,7 @@ static int32_t run_pipeline_impl(hawk_ctx* ctx, const hawk_pipeline* pipe, const
   if (p.sink == HAWK_SINK_HASH_PUT) {
     st = cuckoo_check(ctx, &p.sink_table, d_flags);
     if (st != HAWK_OK) return st;
-    if (p.sink_table.d_index != nullptr) {  // filled entries of the dense index (ctrl word 7)
+    if (p.sink_table.d_index != nullptr && !kp.index_atomic) {  // filled entries of the dense index (ctrl word 7)
       HK_TRY(cudaMemsetAsync(ctx->d_ctrl + 7, 0, 8, ctx->stream));
       hk::index_fill_count_kernel<<<grid_for(ctx, std::max<int64_t>(p.sink_table.index_span / 4, 1), 256), 256, 0,
                                     ctx->stream>>>(p.sink_table.d_index, p.sink_table.index_span, ctx->d_ctrl + 7);
@@ -1374,7 +1385,8 @@ static int32_t run_pipeline_impl(hawk_ctx* ctx, const hawk_pipeline* pipe, const
     }
   }
   if (deferred) {  // the verdict stays on the device until hawk_b200_deferred_collect
-    hk::build_verdict_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_ctrl, p.sink_table.d_index != nullptr ? 1 : 0,
+    hk::build_verdict_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_ctrl,
+                                                       p.sink_table.d_index != nullptr && !kp.index_atomic ? 1 : 0,
                                                        ctx->d_verdicts + 4 * deferred_slot);
     HK_TRY(cudaGetLastError());
     HK_TRY(cudaEventRecord(ev_end, ctx->stream));
@@ -1458,7 +1470,8 @@ static int32_t run_pipeline_impl(hawk_ctx* ctx, const hawk_pipeline* pipe, const
       out->rows = s == HAWK_MULTI_PASS ? rows_written : (int64_t)ctrl[2];
       // a dense index holds one entry per distinct key: fewer filled entries
       // than inserted rows means a duplicate build key
-      if (p.sink_table.d_index != nullptr && (int64_t)ctrl[7] != out->rows) out->flags |= HAWK_FLAG_DUPLICATE;
+      if (p.sink_table.d_index != nullptr && !kp.index_atomic && (int64_t)ctrl[7] != out->rows)
+        out->flags |= HAWK_FLAG_DUPLICATE;
       break;
   }
   if (metrics) {

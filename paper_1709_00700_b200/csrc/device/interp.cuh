@@ -92,6 +92,8 @@ struct KParams {
   int32_t split_drain;                //   ... queued rows per lane per drain
   int32_t split_bits;                 //   ... key bitmaps for semi-join probes: 1 first, 2 all
   int32_t checked;                    // compiled: device bounds checks (HK_CHECKED)
+  int32_t index_atomic;               // compiled single-pass builds: dense-index inserts by
+                                      //   atomic exchange, duplicates flagged in place (HK_INDEX_ATOMIC)
   int32_t smem_state_off;
   int32_t state_words;                // state words per thread
   int32_t rid_base, key_base, acc_base;
