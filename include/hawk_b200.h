@@ -283,7 +283,11 @@ int32_t hawk_b200_ctx_synchronize(hawk_ctx* ctx);
  * "min_ctas" (compiled: __launch_bounds__ minimum CTAs per SM; 0 = by unroll),
  * "priv_groups" (HASH_AGGREGATE local: groups with thread-private accumulators),
  * "checked" (compiled programs carry device-side bounds checks on every
- * indexed access; a failure raises HAWK_FLAG_CHECK). */
+ * indexed access; a failure raises HAWK_FLAG_CHECK),
+ * "graphs" (a pipeline's stream work is captured once per launch
+ * configuration into a CUDA graph and replayed; default 1),
+ * "index_atomic" (compiled single-pass builds into dense indexes of <= 2^21
+ * entries insert by atomic exchange instead of a count pass; default 1). */
 int32_t hawk_b200_ctx_set_option(hawk_ctx* ctx, const char* name, int64_t value);
 /* Reads an option back ("dense_join": 1 = join builds over a dense key range
  * use a direct-addressed index instead of the variant's hash table; default 1). */

@@ -3,6 +3,8 @@
 // one lowered pipeline: strategy -> kernel roles, launch shapes, shared-memory
 // layout, multi-pass orchestration, result/flag read-back.
 #include <chrono>
+#include <string>
+#include <unordered_map>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -68,6 +70,15 @@ struct hawk_ctx {
   int def_launches[HAWK_MAX_DEFERRED] = {};
   int def_pending = 0;  // slots launched since the last collect
   cudaEvent_t ev_col[HAWK_MAX_WIDTH] = {};  // per-column read-back completion (rows_pack_fetch)
+  // option "graphs": a pipeline's stream work, captured once per launch
+  // configuration and replayed with one cudaGraphLaunch (TPC-H Q1 SF10
+  // 0.597 -> 0.590 ms per query, profiles/ab_r02_graphs.txt)
+  int graphs = 1;
+  struct Graph {
+    cudaGraphExec_t exec;
+    int launches;
+  };
+  std::unordered_map<std::string, Graph> graph_cache;
   int def_ready = 0;    // slots whose verdicts rode on a pipeline's read-back
 };
 
@@ -557,6 +568,7 @@ int32_t hawk_b200_ctx_destroy(hawk_ctx* ctx) {
       if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->ev_col)
     if (e) cudaEventDestroy(e);
+  for (auto& kv : ctx->graph_cache) cudaGraphExecDestroy(kv.second.exec);
   cudaEventDestroy(ctx->ev0);
   cudaEventDestroy(ctx->ev1);
   cudaStreamDestroy(ctx->stream);
@@ -673,6 +685,10 @@ int32_t hawk_b200_ctx_set_option(hawk_ctx* ctx, const char* name, int64_t value)
     ctx->checked = value != 0;
     return HAWK_OK;
   }
+  if (std::strcmp(name, "graphs") == 0) {
+    ctx->graphs = value != 0;
+    return HAWK_OK;
+  }
   if (std::strcmp(name, "index_atomic") == 0) {
     ctx->index_atomic = value != 0;
     return HAWK_OK;
@@ -696,7 +712,8 @@ int32_t hawk_b200_ctx_get_option(hawk_ctx* ctx, const char* name, int64_t* value
       {"stage_probes", ctx->stage_probes}, {"pass_sync", ctx->pass_sync}, {"jit", ctx->jit},
       {"stage", ctx->stage}, {"priv_groups", ctx->priv_groups}, {"dense_join", ctx->dense_join},
       {"drain_rows", ctx->drain_rows}, {"split_bits", ctx->split_bits},
-      {"checked", ctx->checked}, {"index_atomic", ctx->index_atomic}};
+      {"checked", ctx->checked}, {"index_atomic", ctx->index_atomic},
+      {"graphs", ctx->graphs}};
   for (const auto& o : opts)
     if (std::strcmp(name, o.n) == 0) {
       *value = o.v;
@@ -1338,98 +1355,166 @@ static int32_t run_pipeline_impl(hawk_ctx* ctx, const hawk_pipeline* pipe, const
   }
 
   const double t_prepare = trace ? us_since(t_start) : 0.0;
-  HK_TRY(cudaMemcpyAsync(ctx->d_ctrl, ctx->h_upload, upload_words * 8, cudaMemcpyHostToDevice, ctx->stream));
   const bool deferred = deferred_slot >= 0;
   cudaEvent_t ev_begin = deferred ? ctx->ev_def[deferred_slot][0] : ctx->ev0;
   cudaEvent_t ev_end = deferred ? ctx->ev_def[deferred_slot][1] : ctx->ev1;
-  HK_TRY(cudaEventRecord(ev_begin, ctx->stream));
-  const double t_upload = trace ? us_since(t_start) : 0.0;
-  double t_first_launch = 0.0;
+  // HASH_AGGREGATE with a host buffer: compact the groups right behind the
+  // pipeline and read up to h_cap_rows of them back with the control words,
+  // so small group-bys (TPC-H Q1: 4 groups) finish with one synchronisation
+  const bool extract = !deferred && h_rows != nullptr && p.sink == HAWK_SINK_HASH_AGGREGATE;
+  int64_t ex_width = 0, ex_copied = 0, ex_slots = 0;
+  if (extract) {
+    const hawk_table& t = p.sink_table;
+    ex_width = p.nkeys + p.naggs;
+    ex_slots = t.capacity * (t.impl == HAWK_CUCKOO ? 2 : 1);
+    st = ensure(ctx->d_groups, ctx->groups_cap, (size_t)ex_slots * ex_width * 8);
+    if (st != HAWK_OK) return st;
+    ex_copied = std::min(h_cap_rows, ex_slots);
+  }
+  // one synchronising read-back: the control words and, for AGGREGATE, the
+  // accumulators themselves (pinned), plus the verdicts of deferred builds
+  u64* ctrl = ctx->h_readback;
+  const size_t readback_words = 8 + (p.sink == HAWK_SINK_AGGREGATE ? (size_t)p.naggs : 0);
+  const int verdicts = deferred ? 0 : ctx->def_pending;
+  double t_upload = 0.0, t_first_launch = 0.0;
   int nlaunch = 0;
-  if (s == HAWK_MULTI_PASS) {
-    // pass 1: per-CTA counts; pass 2: exclusive scan; pass 3: scatter
-    st = launch(ctx, hk::K_COUNT, *v, kp, count_shape);
-    if (st != HAWK_OK) return st;
-    hk::scan_single_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->d_offsets, shape.grid.x, d_total);
-    HK_TRY(cudaGetLastError());
-    st = launch(ctx, hk::K_PROJECT_SCATTER, *v, kp2, shape);
-    if (st != HAWK_OK) return st;
-    nlaunch = 3;
-  } else {
-    for (const Launch& l : launches) {
-      st = launch(ctx, l.role, *v, kp, l.shape);
-      if (st != HAWK_OK) return st;
-      if (trace && nlaunch == 0) t_first_launch = us_since(t_start);
-      ++nlaunch;
-    }
-  }
   int64_t rows_written = -1;
-  if (s == HAWK_MULTI_PASS) {
-    HK_TRY(cudaMemcpyAsync(&rows_written, d_total, 8, cudaMemcpyDeviceToHost, ctx->stream));
-    HK_TRY(cudaStreamSynchronize(ctx->stream));
-    if (p.sink == HAWK_SINK_HASH_PUT) {
-      st = insert_launch(ctx, &p.sink_table, ctx->d_out, ctx->d_out + out_stride, rows_written,
-                         d_flags);
-      if (st != HAWK_OK) return st;
-      ++nlaunch;
-    }
-  }
-  if (p.sink == HAWK_SINK_HASH_PUT) {
-    st = cuckoo_check(ctx, &p.sink_table, d_flags);
-    if (st != HAWK_OK) return st;
-    if (p.sink_table.d_index != nullptr && !kp.index_atomic) {  // filled entries of the dense index (ctrl word 7)
-      HK_TRY(cudaMemsetAsync(ctx->d_ctrl + 7, 0, 8, ctx->stream));
-      hk::index_fill_count_kernel<<<grid_for(ctx, std::max<int64_t>(p.sink_table.index_span / 4, 1), 256), 256, 0,
-                                    ctx->stream>>>(p.sink_table.d_index, p.sink_table.index_span, ctx->d_ctrl + 7);
+  bool capturing = false;
+  auto record = [&](cudaEvent_t e) {  // event nodes of a captured graph must be external
+    return capturing ? cudaEventRecordWithFlags(e, ctx->stream, cudaEventRecordExternal)
+                     : cudaEventRecord(e, ctx->stream);
+  };
+  // everything the pipeline puts on the stream, from the control-word upload
+  // to the read-back (captured once per launch configuration into a CUDA
+  // graph when the "graphs" option is on; see graph_key)
+  auto enqueue = [&]() -> int32_t {
+    nlaunch = 0;
+    HK_TRY(cudaMemcpyAsync(ctx->d_ctrl, ctx->h_upload, upload_words * 8, cudaMemcpyHostToDevice, ctx->stream));
+    HK_TRY(record(ev_begin));
+    if (trace) t_upload = us_since(t_start);
+    int32_t st2 = HAWK_OK;
+    if (s == HAWK_MULTI_PASS) {
+      // pass 1: per-CTA counts; pass 2: exclusive scan; pass 3: scatter
+      st2 = launch(ctx, hk::K_COUNT, *v, kp, count_shape);
+      if (st2 != HAWK_OK) return st2;
+      hk::scan_single_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->d_offsets, shape.grid.x, d_total);
       HK_TRY(cudaGetLastError());
+      st2 = launch(ctx, hk::K_PROJECT_SCATTER, *v, kp2, shape);
+      if (st2 != HAWK_OK) return st2;
+      nlaunch = 3;
+    } else {
+      for (const Launch& l : launches) {
+        st2 = launch(ctx, l.role, *v, kp, l.shape);
+        if (st2 != HAWK_OK) return st2;
+        if (trace && nlaunch == 0) t_first_launch = us_since(t_start);
+        ++nlaunch;
+      }
     }
+    if (s == HAWK_MULTI_PASS) {
+      HK_TRY(cudaMemcpyAsync(&rows_written, d_total, 8, cudaMemcpyDeviceToHost, ctx->stream));
+      HK_TRY(cudaStreamSynchronize(ctx->stream));
+      if (p.sink == HAWK_SINK_HASH_PUT) {
+        st2 = insert_launch(ctx, &p.sink_table, ctx->d_out, ctx->d_out + out_stride, rows_written, d_flags);
+        if (st2 != HAWK_OK) return st2;
+        ++nlaunch;
+      }
+    }
+    if (p.sink == HAWK_SINK_HASH_PUT) {
+      st2 = cuckoo_check(ctx, &p.sink_table, d_flags);
+      if (st2 != HAWK_OK) return st2;
+      if (p.sink_table.d_index != nullptr && !kp.index_atomic) {  // filled entries of the dense index (ctrl word 7)
+        HK_TRY(cudaMemsetAsync(ctx->d_ctrl + 7, 0, 8, ctx->stream));
+        hk::index_fill_count_kernel<<<grid_for(ctx, std::max<int64_t>(p.sink_table.index_span / 4, 1), 256), 256,
+                                      0, ctx->stream>>>(p.sink_table.d_index, p.sink_table.index_span,
+                                                        ctx->d_ctrl + 7);
+        HK_TRY(cudaGetLastError());
+      }
+    }
+    if (deferred) {  // the verdict stays on the device until hawk_b200_deferred_collect
+      hk::build_verdict_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_ctrl,
+                                                         p.sink_table.d_index != nullptr && !kp.index_atomic ? 1 : 0,
+                                                         ctx->d_verdicts + 4 * deferred_slot);
+      HK_TRY(cudaGetLastError());
+      HK_TRY(record(ev_end));
+      return HAWK_OK;
+    }
+    HK_TRY(record(ev_end));
+    if (extract) {
+      HK_TRY(cudaMemsetAsync(ctx->d_ctrl + 7, 0, 8, ctx->stream));
+      hk::agg_extract_kernel<<<grid_for(ctx, ex_slots, 256), 256, 0, ctx->stream>>>(
+          reinterpret_cast<const u64*>(p.sink_table.d_slots), ex_slots, p.nkeys, p.naggs, ctx->d_groups,
+          ctx->d_ctrl + 7);
+      HK_TRY(cudaGetLastError());
+      ++nlaunch;
+      if (ex_copied > 0)
+        HK_TRY(cudaMemcpyAsync(h_rows, ctx->d_groups, (size_t)ex_copied * ex_width * 8, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+    }
+    HK_TRY(cudaMemcpyAsync(ctrl, ctx->d_ctrl, readback_words * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    if (verdicts > 0)  // verdicts of the deferred builds ride on the same synchronisation
+      HK_TRY(cudaMemcpyAsync(ctx->h_verdicts, ctx->d_verdicts, (size_t)verdicts * 4 * 8, cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    return HAWK_OK;
+  };
+  const bool graphed = ctx->graphs && !deferred && !trace && s != HAWK_MULTI_PASS;
+  if (graphed) {
+    // the key: every value the enqueued work depends on (the kernel
+    // parameters hold all device pointers and sizes)
+    std::string key;
+    auto put = [&](const void* d, size_t n) { key.append(static_cast<const char*>(d), n); };
+    const int64_t hdr[] = {role, (int64_t)upload_words, (int64_t)readback_words, verdicts, extract, ex_width,
+                           ex_copied, ex_slots, (int64_t)(uintptr_t)h_rows, (int64_t)(uintptr_t)ctx->d_groups,
+                           (int64_t)launches.size(), p.sink, kp.index_atomic};
+    put(hdr, sizeof hdr);
+    put(&kp, sizeof kp);
+    for (const Launch& l : launches) {
+      put(&l.role, sizeof l.role);
+      put(&l.shape.grid, sizeof l.shape.grid);
+      put(&l.shape.block, sizeof l.shape.block);
+      put(&l.shape.smem, sizeof l.shape.smem);
+      put(&l.shape.jit_fn, sizeof l.shape.jit_fn);
+    }
+    put(v, sizeof *v);
+    put(&p.sink_table, sizeof p.sink_table);
+    auto it = ctx->graph_cache.find(key);
+    if (it == ctx->graph_cache.end()) {
+      if (ctx->graph_cache.size() >= 64) {  // bounded: drop everything and start over
+        for (auto& kv : ctx->graph_cache) cudaGraphExecDestroy(kv.second.exec);
+        ctx->graph_cache.clear();
+      }
+      HK_TRY(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      capturing = true;
+      const int32_t est = enqueue();
+      capturing = false;
+      cudaGraph_t g = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(ctx->stream, &g);
+      if (est != HAWK_OK) {
+        if (g) cudaGraphDestroy(g);
+        return est;
+      }
+      HK_TRY(ce);
+      hawk_ctx::Graph gr{};
+      const cudaError_t ie = cudaGraphInstantiate(&gr.exec, g, 0);
+      cudaGraphDestroy(g);
+      HK_TRY(ie);
+      gr.launches = nlaunch;
+      it = ctx->graph_cache.emplace(std::move(key), gr).first;
+    }
+    nlaunch = it->second.launches;
+    HK_TRY(cudaGraphLaunch(it->second.exec, ctx->stream));
+  } else {
+    st = enqueue();
+    if (st != HAWK_OK) return st;
   }
-  if (deferred) {  // the verdict stays on the device until hawk_b200_deferred_collect
-    hk::build_verdict_kernel<<<1, 1, 0, ctx->stream>>>(ctx->d_ctrl,
-                                                       p.sink_table.d_index != nullptr && !kp.index_atomic ? 1 : 0,
-                                                       ctx->d_verdicts + 4 * deferred_slot);
-    HK_TRY(cudaGetLastError());
-    HK_TRY(cudaEventRecord(ev_end, ctx->stream));
+  if (deferred) {
     ctx->def_launches[deferred_slot] = nlaunch + 1;
     ctx->def_pending = std::max(ctx->def_pending, deferred_slot + 1);
     ctx->def_ready = 0;
     return HAWK_OK;
   }
-  HK_TRY(cudaEventRecord(ev_end, ctx->stream));
-  // HASH_AGGREGATE with a host buffer: compact the groups right behind the
-  // pipeline and read up to h_cap_rows of them back with the control words,
-  // so small group-bys (TPC-H Q1: 4 groups) finish with one synchronisation
-  const bool extract = h_rows != nullptr && p.sink == HAWK_SINK_HASH_AGGREGATE;
-  int64_t ex_width = 0, ex_copied = 0;
-  if (extract) {
-    const hawk_table& t = p.sink_table;
-    const int K = p.nkeys, A = p.naggs;
-    ex_width = K + A;
-    const int64_t nslots = t.capacity * (t.impl == HAWK_CUCKOO ? 2 : 1);
-    st = ensure(ctx->d_groups, ctx->groups_cap, (size_t)nslots * ex_width * 8);
-    if (st != HAWK_OK) return st;
-    HK_TRY(cudaMemsetAsync(ctx->d_ctrl + 7, 0, 8, ctx->stream));
-    hk::agg_extract_kernel<<<grid_for(ctx, nslots, 256), 256, 0, ctx->stream>>>(
-        reinterpret_cast<const u64*>(t.d_slots), nslots, K, A, ctx->d_groups, ctx->d_ctrl + 7);
-    HK_TRY(cudaGetLastError());
-    ++nlaunch;
-    ex_copied = std::min(h_cap_rows, nslots);
-    if (ex_copied > 0)
-      HK_TRY(cudaMemcpyAsync(h_rows, ctx->d_groups, (size_t)ex_copied * ex_width * 8, cudaMemcpyDeviceToHost,
-                             ctx->stream));
-  }
+  if (verdicts > 0) ctx->def_ready = verdicts;
   const double t_launch = trace ? us_since(t_start) : 0.0;
   const double t_first = t_first_launch;
-  // one synchronising read-back: the control words and, for AGGREGATE, the
-  // accumulators themselves (pinned)
-  u64* ctrl = ctx->h_readback;
-  const size_t readback_words = 8 + (p.sink == HAWK_SINK_AGGREGATE ? (size_t)p.naggs : 0);
-  HK_TRY(cudaMemcpyAsync(ctrl, ctx->d_ctrl, readback_words * 8, cudaMemcpyDeviceToHost, ctx->stream));
-  if (ctx->def_pending > 0) {  // verdicts of the deferred builds ride on the same synchronisation
-    HK_TRY(cudaMemcpyAsync(ctx->h_verdicts, ctx->d_verdicts, (size_t)ctx->def_pending * 4 * 8,
-                           cudaMemcpyDeviceToHost, ctx->stream));
-    ctx->def_ready = ctx->def_pending;
-  }
   HK_TRY(stream_wait(ctx->stream));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);

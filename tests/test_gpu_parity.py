@@ -870,3 +870,24 @@ def test_random_queries_match_oracle(micro, seed):
                     assert diff is None, f"seed {seed} #{i} jit={jit} {sql} [{cfg}]: {diff}"
     finally:
         engine.set_option("jit", 0)
+
+
+def test_graph_replay_matches_oracle(bench_db):
+    # option "graphs": each pipeline's stream work is captured once per launch
+    # configuration and replayed; repeated runs (replays), a second variant
+    # (a new capture) and both program modes give the oracle's rows
+    which, engine, db = bench_db
+    engine.set_option("graphs", 1)  # the default; the other tests run with it too
+    try:
+        for key, sql in harness.BENCH:
+            if key.startswith("ssb") != (which == "ssb"):
+                continue
+            want = db.execute(sql)
+            for jit in (1, 0):
+                engine.set_option("jit", jit)
+                for cfg in (CONFIGS[0], CONFIGS[1]):
+                    for _ in range(3):
+                        diff = harness.compare(want, engine.run(sql, cfg))
+                        assert diff is None, f"{key} graphs jit={jit} [{cfg}]: {diff}"
+    finally:
+        engine.set_option("jit", 1)
