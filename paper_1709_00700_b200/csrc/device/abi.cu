@@ -1456,7 +1456,7 @@ static int32_t run_pipeline_impl(hawk_ctx* ctx, const hawk_pipeline* pipe, const
                              ctx->stream));
     return HAWK_OK;
   };
-  const bool graphed = ctx->graphs && !deferred && !trace && s != HAWK_MULTI_PASS;
+  const bool graphed = ctx->graphs && !trace && s != HAWK_MULTI_PASS;
   if (graphed) {
     // the key: every value the enqueued work depends on (the kernel
     // parameters hold all device pointers and sizes)
@@ -1464,7 +1464,7 @@ static int32_t run_pipeline_impl(hawk_ctx* ctx, const hawk_pipeline* pipe, const
     auto put = [&](const void* d, size_t n) { key.append(static_cast<const char*>(d), n); };
     const int64_t hdr[] = {role, (int64_t)upload_words, (int64_t)readback_words, verdicts, extract, ex_width,
                            ex_copied, ex_slots, (int64_t)(uintptr_t)h_rows, (int64_t)(uintptr_t)ctx->d_groups,
-                           (int64_t)launches.size(), p.sink, kp.index_atomic};
+                           (int64_t)launches.size(), p.sink, kp.index_atomic, deferred_slot};
     put(hdr, sizeof hdr);
     put(&kp, sizeof kp);
     for (const Launch& l : launches) {
