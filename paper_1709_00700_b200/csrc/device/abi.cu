@@ -367,6 +367,21 @@ bool split_rows_for(const hawk_pipeline& pipe, const hawk_variant& v, int role) 
          (role <= hk::K_HAGG_GLOBAL || role == hk::K_PROJECT_SINGLE);
 }
 
+// __launch_bounds__ minimum CTAs/SM of a compiled program when the option
+// does not set one (0 = by unroll: 3 / 2 / 1 for u = 1 / 2 / 4):
+// - thread-private group-by accumulators: 2 (0.79 -> 0.67 ms on TPC-H Q1 SF10,
+//   profiles/ab_r02_q1_min_ctas.txt);
+// - global-hash group-by at u = 1: 4, i.e. <= 64 registers, for more loads in
+//   flight behind the probe chain (TPC-H Q3 SF100 terminal 3.21 -> 2.88 ms);
+// - single-pass builds at u = 4: 2 instead of 1 (Q3 SF100 orders build 0.92 ->
+//   0.69 ms; profiles/ab_r02_min_ctas_roles.txt).
+static int auto_min_ctas(int role, const hawk_variant& v, bool priv) {
+  if (priv) return 2;
+  if (role == hk::K_HAGG_GLOBAL && v.unroll_factor == 1) return 4;
+  if (role == hk::K_PUT_SINGLE && v.unroll_factor == 4) return 2;
+  return 0;
+}
+
 int32_t prepare(hawk_ctx* ctx, const hawk_pipeline& pipe, const hawk_variant& v, int role,
                 int block, int64_t grid_or_zero, int64_t per_sm_cap, hk::KParams& kp,
                 hk::LaunchShape& shape) {
@@ -412,7 +427,7 @@ int32_t prepare(hawk_ctx* ctx, const hawk_pipeline& pipe, const hawk_variant& v,
   // 0.67 vs 0.79 ms on Q1 SF10 (profiles/ab_r02_q1_min_ctas.txt)
   const bool priv = role == hk::K_HAGG_LOCAL && pipe.naggs > 0 &&
                     (ctx->priv_groups >= 0 ? ctx->priv_groups > 0 : pipe.nprobe == 0);
-  kp.min_ctas = ctx->min_ctas > 0 ? ctx->min_ctas : (priv && ctx->jit ? 2 : 0);
+  kp.min_ctas = ctx->min_ctas > 0 ? ctx->min_ctas : ctx->jit ? auto_min_ctas(role, v, priv) : 0;
   shape.jit_fn = nullptr;
   if (ctx->jit) {  // compiled program: generate + NVRTC (cached), see jit.cu
     std::string err;
@@ -601,7 +616,7 @@ static void program_params(const hawk_pipeline& p, const hawk_variant& v, hk::KP
   kp.split_drain = kp.split ? auto_drain(p) : 1;
   // as prepare() with the default options: private-accumulator group-bys run 2 CTAs/SM
   const int role = main_role(p, v);
-  kp.min_ctas = role == hk::K_HAGG_LOCAL && p.naggs > 0 && p.nprobe == 0 ? 2 : 0;
+  kp.min_ctas = auto_min_ctas(role, v, role == hk::K_HAGG_LOCAL && p.naggs > 0 && p.nprobe == 0);
   kp.checked = std::getenv("HAWK_CHECKED") != nullptr;  // compile-check the instrumented programs
   kp.split_bits = kp.split ? 1 : 0;
   kp.npre = compile_filters(p.filter, p.nfilter, kp.pre);
