@@ -371,13 +371,14 @@ bool split_rows_for(const hawk_pipeline& pipe, const hawk_variant& v, int role) 
 // does not set one (0 = by unroll: 3 / 2 / 1 for u = 1 / 2 / 4):
 // - thread-private group-by accumulators: 2 (0.79 -> 0.67 ms on TPC-H Q1 SF10,
 //   profiles/ab_r02_q1_min_ctas.txt);
-// - global-hash group-by at u = 1: 4, i.e. <= 64 registers, for more loads in
-//   flight behind the probe chain (TPC-H Q3 SF100 terminal 3.21 -> 2.88 ms);
+// - shared-table / global-hash group-by at u = 1: 4, i.e. <= 64 registers, for
+//   more loads in flight behind the probe chain (TPC-H Q3 SF100 terminal
+//   3.21 -> 2.88 ms, SSB Q4.1 SF100 terminal 4.50 -> 4.09 ms);
 // - single-pass builds at u = 4: 2 instead of 1 (Q3 SF100 orders build 0.92 ->
 //   0.69 ms; profiles/ab_r02_min_ctas_roles.txt).
 static int auto_min_ctas(int role, const hawk_variant& v, bool priv) {
   if (priv) return 2;
-  if (role == hk::K_HAGG_GLOBAL && v.unroll_factor == 1) return 4;
+  if ((role == hk::K_HAGG_GLOBAL || role == hk::K_HAGG_LOCAL) && v.unroll_factor == 1) return 4;
   if (role == hk::K_PUT_SINGLE && v.unroll_factor == 4) return 2;
   return 0;
 }
